@@ -1,0 +1,135 @@
+/*
+ * tcbf.h -- C ABI of the B200-native Tensor-Core Beamformer hot path.
+ *
+ * Operation (Sec. II, Eq. 3 mapped to a GEMM): for every batch
+ * entry b ("batch size option"; PAPER.md:393 batch = polarizations
+ * x channels)
+ *
+ *     C[b] = W[b] . X[b]        W: M beams x K receivers,  X: K receivers x N samples
+ *
+ * over complex numbers, in one of two modes (Table I):
+ *   TCBF_PREC_F16  inputs rounded to fp16 (RNE), fp32 accumulate, fp32 output.
+ *                  Complex product as four real sub-GEMMs with one negation
+ *                  (Sec. III-B).
+ *   TCBF_PREC_B1   inputs sign-quantised to one bit per component (bit 1 = +1,
+ *                  bit 0 = -1; value >= 0 -> 1, NaN -> 0; Fig. 1
+ *                  PAPER.md:209-210), exact int32 output equal to the complex dot
+ *                  product over the logical K (Eq. 4-5 with the
+ *                  padded-K reading R1 of DESIGN.md).
+ *
+ * All calls are host functions.  Data pointers are CALLER-OWNED DEVICE pointers
+ * on the device that was current at tcbf_plan_create; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  Calls are asynchronous on the
+ * stream, never modify their inputs, never abort and never throw:
+ * every failure is a tcbf_status, with detail in tcbf_last_error() (thread-local).
+ *
+ * Layouts (row-major, innermost last):
+ *   fp32 sources    weights  W: interleaved [B][M][K] float2 | planar [B][2][M][K]
+ *                   data     X: interleaved [B][K][N] float2 | planar [B][2][K][N]
+ *   packed F16      weights  [B][2][M][Kp] fp16,  data (transposed) [B][2][N][Kp] fp16
+ *                   Kp = round_up(K, 64); K padding is 0.0.
+ *   packed B1       weights  [B][2][M][Kp] uint32, data (transposed) [B][2][N][Kp] uint32
+ *                   Kp = round_up(ceil(K/32), 8) words; bit k%32 of word k/32 is
+ *                   element k (LSB-first, reading R3); padding bits are 0.
+ *   output          [B][2][M][N]  (plane 0 = Re, plane 1 = Im), fp32 (F16) or int32 (B1).
+ * Plane [.][0] holds real parts, [.][1] imaginary parts (PAPER.md:414 re/im separation).
+ */
+#ifndef TCBF_H_
+#define TCBF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  TCBF_OK = 0,
+  TCBF_ERR_INVALID_ARG = 1,        /* bad size, null/misaligned pointer, bad enum */
+  TCBF_ERR_UNSUPPORTED_DEVICE = 2, /* no device, or compute capability != 10.0 (sm_100a) */
+  TCBF_ERR_DEVICE_MISMATCH = 3,    /* current device differs from the plan's device */
+  TCBF_ERR_ALLOC = 4,              /* host or device allocation failed */
+  TCBF_ERR_CUDA = 5                /* CUDA runtime/driver error; text in tcbf_last_error() */
+} tcbf_status;
+
+typedef enum { TCBF_PREC_F16 = 0, TCBF_PREC_B1 = 1 } tcbf_precision;
+typedef enum { TCBF_WEIGHTS = 0, TCBF_DATA = 1 } tcbf_operand;
+typedef enum { TCBF_SRC_INTERLEAVED = 0, TCBF_SRC_PLANAR = 1 } tcbf_src_layout;
+
+typedef struct tcbf_plan_s tcbf_plan;
+
+/* Host-only layout arithmetic (no device needed).  Any output pointer may be NULL.
+ * w_bytes / x_bytes: packed weight / data buffer sizes; out_bytes: output size;
+ * k_packed: Kp (fp16 elements for F16, uint32 words for B1).
+ * Errors: INVALID_ARG if M, N, K, batch < 1, if a size overflows size_t, or if
+ * B1 and K >= 2^30 (|Re|,|Im| <= 2K must fit int32). */
+tcbf_status tcbf_layout_sizes(int64_t M, int64_t N, int64_t K, int64_t batch,
+                              tcbf_precision precision, size_t* w_bytes, size_t* x_bytes,
+                              size_t* out_bytes, int64_t* k_packed);
+
+/* Create an immutable plan for batch x (M beams, N samples, K receivers).
+ * Host-only validation as tcbf_layout_sizes, then binds the current device,
+ * which must be compute capability 10.0 (else UNSUPPORTED_DEVICE).  *plan is
+ * set to NULL on failure.  The plan owns only host metadata. */
+tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, int64_t batch,
+                             tcbf_precision precision);
+
+/* Free a plan.  NULL is a no-op returning TCBF_OK.  Must not race with calls using it. */
+tcbf_status tcbf_plan_destroy(tcbf_plan* plan);
+
+/* Sizes of the plan's packed operand / output buffers in bytes. */
+tcbf_status tcbf_packed_bytes(const tcbf_plan* plan, tcbf_operand operand, size_t* bytes);
+tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes);
+
+/* Pack one operand ("32 consecutive 1-bit samples must be stored in a
+ * single 32-bit integer ... the input matrices are tiled in device memory ... transpose
+ * kernel"; PAPER.md:414 re/im separation).
+ *   F16: fp32 -> fp16 round-to-nearest-even (IEEE: overflow -> inf, NaN stays NaN).
+ *   B1:  sign quantisation, bit = (value >= 0).
+ * src: fp32 source in `layout` (see top); dst: packed buffer of tcbf_packed_bytes().
+ * The DATA operand is transposed to N-major/K-contiguous.  src must be 8-byte
+ * aligned (interleaved) or 4-byte aligned (planar); dst 16-byte aligned.
+ * dst and src must not overlap. */
+tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src,
+                      tcbf_src_layout layout, void* dst, void* stream);
+
+/* The beamformer: out = W . X for every batch entry (Eq. 3).
+ * w_packed / x_packed: buffers written by tcbf_pack (16-byte aligned);
+ * out: tcbf_output_bytes() bytes, 16-byte aligned, must not overlap the inputs.
+ * F16: fp32 result of fp16 inputs with fp32 accumulation (tcgen05 tensor cores).
+ * B1:  exact int32 result.  One call may be in flight per (plan, out) pair;
+ * the plan itself is stateless and may be used from several streams. */
+tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed,
+                          void* out, void* stream);
+
+/* End-to-end convenience over HOST buffers (the e2e boundary): copies the fp32
+ * data X (host, pinned recommended) to the device in batch chunks, packs it,
+ * beamforms against the already packed device weights and copies the output back
+ * to `out_host`, overlapping copies and compute on internal streams.  Blocks until
+ * done.  Device scratch is allocated per call (ALLOC on failure). */
+tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_packed_dev,
+                               const float* x_host, tcbf_src_layout layout, void* out_host);
+
+/* Number of kernel launches the last tcbf_beamform / tcbf_pack call on this thread
+ * issued (for launch accounting in benchmarks). */
+int tcbf_last_launch_count(void);
+
+/* Name of the kernel variant the plan dispatches to (static string). */
+const char* tcbf_plan_variant(const tcbf_plan* plan);
+
+const char* tcbf_status_string(tcbf_status status);
+const char* tcbf_last_error(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCBF_H_ */

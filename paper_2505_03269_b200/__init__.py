@@ -1,0 +1,164 @@
+"""paper_2505_03269_b200 -- B200-native Tensor-Core Beamformer hot path.
+
+Thin Python binding (argument marshalling only) of the C ABI in include/tcbf.h,
+implemented by lib/libtcbf.so (hand-written sm_100a CUDA).  Every step of the
+path -- packing, the complex GEMM, the epilogue -- runs in those kernels; torch is
+used only to own device memory and streams.  There is NO CPU fallback: if the
+native library is missing this module raises.
+
+    plan = Plan(M, N, K, batch, "f16" | "b1")
+    wp = plan.pack(WEIGHTS, w)            # w: cuda float32 [B,M,K,2] or [B,2,M,K]
+    xp = plan.pack(DATA, x)               # x: cuda float32 [B,K,N,2] or [B,2,K,N]
+    y  = plan.beamform(wp, xp)            # [B,2,M,N] float32 (f16) / int32 (b1)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["Plan", "TcbfError", "layout_sizes", "WEIGHTS", "DATA", "INTERLEAVED", "PLANAR",
+           "F16", "B1", "library_path", "lib"]
+
+F16, B1 = 0, 1
+WEIGHTS, DATA = 0, 1
+INTERLEAVED, PLANAR = 0, 1
+_PREC = {"f16": F16, "b1": B1, F16: F16, B1: B1}
+_LAYOUT = {"interleaved": INTERLEAVED, "planar": PLANAR, INTERLEAVED: INTERLEAVED, PLANAR: PLANAR}
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "lib", "libtcbf.so")
+
+
+class TcbfError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        super().__init__(f"{where}: {status_string(status)}: {detail}")
+        self.status = status
+
+
+_LIB = None
+
+
+def lib():
+    """The loaded libtcbf.so (raises if it was not built -- no fallback path)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(library_path):
+            raise RuntimeError(f"native library missing: {library_path}; run __graft_entry__.build()")
+        L = ctypes.CDLL(library_path)
+        i64, vp, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+        L.tcbf_layout_sizes.restype = ctypes.c_int
+        L.tcbf_layout_sizes.argtypes = [i64, i64, i64, i64, ctypes.c_int, ctypes.POINTER(sz),
+                                        ctypes.POINTER(sz), ctypes.POINTER(sz), ctypes.POINTER(i64)]
+        L.tcbf_plan_create.restype = ctypes.c_int
+        L.tcbf_plan_create.argtypes = [ctypes.POINTER(vp), i64, i64, i64, i64, ctypes.c_int]
+        L.tcbf_plan_destroy.restype = ctypes.c_int
+        L.tcbf_plan_destroy.argtypes = [vp]
+        L.tcbf_packed_bytes.restype = ctypes.c_int
+        L.tcbf_packed_bytes.argtypes = [vp, ctypes.c_int, ctypes.POINTER(sz)]
+        L.tcbf_output_bytes.restype = ctypes.c_int
+        L.tcbf_output_bytes.argtypes = [vp, ctypes.POINTER(sz)]
+        L.tcbf_pack.restype = ctypes.c_int
+        L.tcbf_pack.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, vp]
+        L.tcbf_beamform.restype = ctypes.c_int
+        L.tcbf_beamform.argtypes = [vp, vp, vp, vp, vp]
+        L.tcbf_beamform_host.restype = ctypes.c_int
+        L.tcbf_beamform_host.argtypes = [vp, vp, vp, ctypes.c_int, vp]
+        L.tcbf_last_launch_count.restype = ctypes.c_int
+        L.tcbf_last_launch_count.argtypes = []
+        L.tcbf_plan_variant.restype = ctypes.c_char_p
+        L.tcbf_plan_variant.argtypes = [vp]
+        L.tcbf_status_string.restype = ctypes.c_char_p
+        L.tcbf_status_string.argtypes = [ctypes.c_int]
+        L.tcbf_last_error.restype = ctypes.c_char_p
+        L.tcbf_last_error.argtypes = []
+        _LIB = L
+    return _LIB
+
+
+def status_string(s: int) -> str:
+    return lib().tcbf_status_string(int(s)).decode()
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise TcbfError(rc, where, lib().tcbf_last_error().decode())
+
+
+def layout_sizes(M, N, K, batch, precision="f16"):
+    """Host-only: (w_bytes, x_bytes, out_bytes, k_packed)."""
+    w, x, o, k = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_int64()
+    _check(lib().tcbf_layout_sizes(M, N, K, batch, _PREC[precision], ctypes.byref(w), ctypes.byref(x),
+                                   ctypes.byref(o), ctypes.byref(k)), "tcbf_layout_sizes")
+    return w.value, x.value, o.value, k.value
+
+
+def _stream_ptr(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """Immutable beamforming plan for `batch` x (M beams, N samples, K receivers)."""
+
+    def __init__(self, M: int, N: int, K: int, batch: int, precision="f16"):
+        self.M, self.N, self.K, self.batch = int(M), int(N), int(K), int(batch)
+        self.precision = _PREC[precision]
+        h = ctypes.c_void_p()
+        _check(lib().tcbf_plan_create(ctypes.byref(h), self.M, self.N, self.K, self.batch, self.precision),
+               "tcbf_plan_create")
+        self._h = h
+        self.w_bytes, self.x_bytes, self.out_bytes, self.k_packed = layout_sizes(
+            self.M, self.N, self.K, self.batch, self.precision)
+        self.variant = lib().tcbf_plan_variant(h).decode()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().tcbf_plan_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # ------------------------------------------------------------ buffers (torch = plumbing)
+    def packed_shape(self, operand):
+        rows = self.M if operand == WEIGHTS else self.N
+        return (self.batch, 2, rows, self.k_packed)
+
+    def alloc_packed(self, operand, device="cuda"):
+        import torch
+        dt = torch.float16 if self.precision == F16 else torch.int32
+        return torch.empty(self.packed_shape(operand), dtype=dt, device=device)
+
+    def alloc_output(self, device="cuda"):
+        import torch
+        dt = torch.float32 if self.precision == F16 else torch.int32
+        return torch.empty((self.batch, 2, self.M, self.N), dtype=dt, device=device)
+
+    # ------------------------------------------------------------ the path
+    def pack(self, operand, src, layout="interleaved", out=None, stream=None):
+        lay = _LAYOUT[layout]
+        if out is None:
+            out = self.alloc_packed(operand, src.device)
+        _check(lib().tcbf_pack(self._h, int(operand), ctypes.c_void_p(src.data_ptr()), lay,
+                               ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream, src.device)), "tcbf_pack")
+        return out
+
+    def beamform(self, w_packed, x_packed, out=None, stream=None):
+        if out is None:
+            out = self.alloc_output(w_packed.device)
+        _check(lib().tcbf_beamform(self._h, ctypes.c_void_p(w_packed.data_ptr()),
+                                   ctypes.c_void_p(x_packed.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                   _stream_ptr(stream, w_packed.device)), "tcbf_beamform")
+        return out
+
+    def beamform_host(self, w_packed_dev, x_host, out_host, layout="interleaved"):
+        """End-to-end over host buffers (torch CPU tensors, pinned for overlap)."""
+        _check(lib().tcbf_beamform_host(self._h, ctypes.c_void_p(w_packed_dev.data_ptr()),
+                                        ctypes.c_void_p(x_host.data_ptr()), _LAYOUT[layout],
+                                        ctypes.c_void_p(out_host.data_ptr())), "tcbf_beamform_host")
+        return out_host
+
+    @staticmethod
+    def last_launch_count() -> int:
+        return lib().tcbf_last_launch_count()

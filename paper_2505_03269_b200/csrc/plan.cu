@@ -1,0 +1,274 @@
+// plan.cu -- the C ABI (include/tcbf.h): validation, layout arithmetic, TMA descriptor
+// encoding and dispatch to the sm_100a kernels.  No exceptions or aborts cross the ABI.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "kernels.h"
+#include "plan_internal.h"
+#include "tcbf.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+tcbf_status fail(tcbf_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+tcbf_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(TCBF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool mul_ok(size_t a, size_t b, size_t* out) {
+  if (a != 0 && b > SIZE_MAX / a) return false;
+  *out = a * b;
+  return true;
+}
+
+tcbf_status compute_sizes(int64_t M, int64_t N, int64_t K, int64_t B, tcbf_precision p, size_t* wb, size_t* xb,
+                          size_t* ob, int64_t* kp) {
+  if (M < 1 || N < 1 || K < 1 || B < 1)
+    return fail(TCBF_ERR_INVALID_ARG, "M, N, K, batch must be >= 1 (got %lld, %lld, %lld, %lld)", (long long)M,
+                (long long)N, (long long)K, (long long)B);
+  if (p != TCBF_PREC_F16 && p != TCBF_PREC_B1) return fail(TCBF_ERR_INVALID_ARG, "unknown precision %d", (int)p);
+  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || B > INT32_MAX)
+    return fail(TCBF_ERR_INVALID_ARG, "dimensions must fit int32");
+  if (p == TCBF_PREC_B1 && K >= (int64_t(1) << 30))
+    return fail(TCBF_ERR_INVALID_ARG, "1-bit mode requires K < 2^30 so |Re|,|Im| <= 2K fit int32");
+  int64_t k = p == TCBF_PREC_F16 ? (K + 63) / 64 * 64 : ((K + 31) / 32 + 7) / 8 * 8;
+  size_t elem = p == TCBF_PREC_F16 ? 2 : 4;
+  size_t t, w, x, o;
+  if (!mul_ok((size_t)B * 2, (size_t)M, &t) || !mul_ok(t, (size_t)k, &t) || !mul_ok(t, elem, &w))
+    return fail(TCBF_ERR_INVALID_ARG, "packed weight size overflows size_t");
+  if (!mul_ok((size_t)B * 2, (size_t)N, &t) || !mul_ok(t, (size_t)k, &t) || !mul_ok(t, elem, &x))
+    return fail(TCBF_ERR_INVALID_ARG, "packed data size overflows size_t");
+  if (!mul_ok((size_t)B * 2, (size_t)M, &t) || !mul_ok(t, (size_t)N, &t) || !mul_ok(t, 4, &o))
+    return fail(TCBF_ERR_INVALID_ARG, "output size overflows size_t");
+  if (wb) *wb = w;
+  if (xb) *xb = x;
+  if (ob) *ob = o;
+  if (kp) *kp = k;
+  return TCBF_OK;
+}
+
+tcbf_status check_device(const tcbf_plan* plan) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev != plan->device)
+    return fail(TCBF_ERR_DEVICE_MISMATCH, "current device %d differs from the plan's device %d", dev, plan->device);
+  return TCBF_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency).
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+tcbf_status encode_3d(CUtensorMap* map, CUtensorMapDataType dt, size_t elem, const void* base, uint64_t d0,
+                      uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1, CUtensorMapSwizzle sw,
+                      CUtensorMapL2promotion l2) {
+  auto enc = get_encode();
+  if (!enc) return fail(TCBF_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * elem, d0 * d1 * elem};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TCBF_ERR_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", (int)r);
+  return TCBF_OK;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+}  // namespace
+
+void tcbf_internal_set_launches(int n) { g_launches = n; }
+
+extern "C" {
+
+tcbf_status tcbf_layout_sizes(int64_t M, int64_t N, int64_t K, int64_t batch, tcbf_precision precision,
+                              size_t* w_bytes, size_t* x_bytes, size_t* out_bytes, int64_t* k_packed) {
+  return compute_sizes(M, N, K, batch, precision, w_bytes, x_bytes, out_bytes, k_packed);
+}
+
+tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, int64_t batch,
+                             tcbf_precision precision) {
+  if (!plan) return fail(TCBF_ERR_INVALID_ARG, "plan out-pointer is NULL");
+  *plan = nullptr;
+  size_t wb, xb, ob;
+  int64_t kp;
+  tcbf_status s = compute_sizes(M, N, K, batch, precision, &wb, &xb, &ob, &kp);
+  if (s != TCBF_OK) return s;
+  int dev = -1, major = 0, minor = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TCBF_ERR_UNSUPPORTED_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(TCBF_ERR_UNSUPPORTED_DEVICE, "cannot query device %d", dev);
+  }
+  if (major != 10 || minor != 0)
+    return fail(TCBF_ERR_UNSUPPORTED_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a", dev, major,
+                minor);
+  tcbf_plan* p = new (std::nothrow) tcbf_plan_s;
+  if (!p) return fail(TCBF_ERR_ALLOC, "host allocation of the plan failed");
+  p->M = M; p->N = N; p->K = K; p->B = batch;
+  p->prec = precision;
+  p->kp = kp;
+  p->device = dev;
+  p->num_sms = sms;
+  p->w_bytes = wb; p->x_bytes = xb; p->out_bytes = ob;
+  // fp16 tile width: BN = 128 unless N is small enough that 64 wastes less (e.g. N <= 64)
+  p->block_n = N <= 64 ? 64 : 128;
+  if (const char* env = getenv("TCBF_F16_BLOCK_N")) {
+    int v = atoi(env);
+    if (v == 64 || v == 128) p->block_n = v;
+  }
+  *plan = p;
+  return TCBF_OK;
+}
+
+tcbf_status tcbf_plan_destroy(tcbf_plan* plan) {
+  delete plan;
+  return TCBF_OK;
+}
+
+tcbf_status tcbf_packed_bytes(const tcbf_plan* plan, tcbf_operand operand, size_t* bytes) {
+  if (!plan || !bytes) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (operand != TCBF_WEIGHTS && operand != TCBF_DATA) return fail(TCBF_ERR_INVALID_ARG, "bad operand");
+  *bytes = operand == TCBF_WEIGHTS ? plan->w_bytes : plan->x_bytes;
+  return TCBF_OK;
+}
+
+tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes) {
+  if (!plan || !bytes) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  *bytes = plan->out_bytes;
+  return TCBF_OK;
+}
+
+const char* tcbf_plan_variant(const tcbf_plan* plan) {
+  if (!plan) return "none";
+  if (plan->prec == TCBF_PREC_B1) return "b1_popc_xor_64x64";
+  if (plan->N % 4 != 0) return plan->block_n == 64 ? "f16_tcgen05_128x64_stg" : "f16_tcgen05_128x128_stg";
+  return plan->block_n == 64 ? "f16_tcgen05_128x64_tma" : "f16_tcgen05_128x128_tma";
+}
+
+tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src, tcbf_src_layout layout,
+                      void* dst, void* stream) {
+  g_launches = 0;
+  if (!plan || !src || !dst) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (operand != TCBF_WEIGHTS && operand != TCBF_DATA) return fail(TCBF_ERR_INVALID_ARG, "bad operand");
+  if (layout != TCBF_SRC_INTERLEAVED && layout != TCBF_SRC_PLANAR) return fail(TCBF_ERR_INVALID_ARG, "bad layout");
+  if (!aligned(src, layout == TCBF_SRC_INTERLEAVED ? 8 : 4) || !aligned(dst, 16))
+    return fail(TCBF_ERR_INVALID_ARG, "misaligned src (needs %d B) or dst (needs 16 B)",
+                layout == TCBF_SRC_INTERLEAVED ? 8 : 4);
+  tcbf_status s = check_device(plan);
+  if (s != TCBF_OK) return s;
+  const int64_t R = operand == TCBF_WEIGHTS ? plan->M : plan->K;
+  const int64_t C = operand == TCBF_WEIGHTS ? plan->K : plan->N;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (plan->prec == TCBF_PREC_F16)
+    e = tcbf::launch_pack_f16(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, static_cast<uint16_t*>(dst), st);
+  else
+    e = tcbf::launch_pack_b1(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, static_cast<uint32_t*>(dst), st);
+  if (e != cudaSuccess) return cuda_fail(e, "pack kernel launch");
+  g_launches = 1;
+  return TCBF_OK;
+}
+
+tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed, void* out, void* stream) {
+  g_launches = 0;
+  if (!plan || !w_packed || !x_packed || !out) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (!aligned(w_packed, 16) || !aligned(x_packed, 16) || !aligned(out, 16))
+    return fail(TCBF_ERR_INVALID_ARG, "packed operands and output must be 16-byte aligned");
+  tcbf_status s = check_device(plan);
+  if (s != TCBF_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (plan->prec == TCBF_PREC_F16) {
+    const int bn = plan->block_n;
+    const bool tma_store = (plan->N % 4) == 0;
+    CUtensorMap ta, tb, tc;
+    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->kp, plan->N, 2 * plan->B, 64, bn,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    if (tma_store) {
+      s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+      if (s != TCBF_OK) return s;
+    } else {
+      memset(&tc, 0, sizeof(tc));
+    }
+    tcbf::GemmF16Args a;
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + 127) / 128);
+    a.tiles_n = (int)((plan->N + bn - 1) / bn);
+    const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
+    if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+    a.num_tiles = (int)nt;
+    a.num_kb = (int)(plan->kp / 64);
+    a.out = static_cast<float*>(out);
+    e = tcbf::launch_gemm_f16(ta, tb, tc, a, bn, tma_store, plan->num_sms, st);
+  } else {
+    tcbf::GemmB1Args a;
+    a.w = static_cast<const uint32_t*>(w_packed);
+    a.x = static_cast<const uint32_t*>(x_packed);
+    a.out = static_cast<int32_t*>(out);
+    a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
+    e = tcbf::launch_gemm_b1_popc(a, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
+  g_launches = 1;
+  return TCBF_OK;
+}
+
+int tcbf_last_launch_count(void) { return g_launches; }
+
+const char* tcbf_status_string(tcbf_status status) {
+  switch (status) {
+    case TCBF_OK: return "TCBF_OK";
+    case TCBF_ERR_INVALID_ARG: return "TCBF_ERR_INVALID_ARG";
+    case TCBF_ERR_UNSUPPORTED_DEVICE: return "TCBF_ERR_UNSUPPORTED_DEVICE";
+    case TCBF_ERR_DEVICE_MISMATCH: return "TCBF_ERR_DEVICE_MISMATCH";
+    case TCBF_ERR_ALLOC: return "TCBF_ERR_ALLOC";
+    case TCBF_ERR_CUDA: return "TCBF_ERR_CUDA";
+  }
+  return "TCBF_ERR_UNKNOWN";
+}
+
+const char* tcbf_last_error(void) { return g_err; }
+
+}  // extern "C"

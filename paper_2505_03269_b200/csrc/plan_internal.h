@@ -1,0 +1,19 @@
+// plan_internal.h -- the plan object behind the opaque tcbf_plan handle (host metadata only).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "tcbf.h"
+
+struct tcbf_plan_s {
+  int64_t M, N, K, B;
+  tcbf_precision prec;
+  int64_t kp;   // K16 (fp16 elements) or Kw (uint32 words)
+  int device;
+  int num_sms;
+  int block_n;  // fp16 GEMM tile width
+  size_t w_bytes, x_bytes, out_bytes;
+};
+
+// launch accounting shared by the ABI entry points (thread-local in plan.cu)
+__attribute__((visibility("hidden"))) void tcbf_internal_set_launches(int n);

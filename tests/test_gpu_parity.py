@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  1-bit: bit-exact.  16-bit: normwise relative error <= 2e-3 per batch
+entry and overall (north_star), plus an elementwise accumulation bound as a diagnostic
+gate, and exact equality where the arithmetic is exact (integer inputs, identity)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F16_TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def tcbf():
+    import paper_2505_03269_b200 as m
+    m.lib()
+    return m
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _rounded(z):
+    return z.real.astype(np.float16).astype(np.float64) + 1j * z.imag.astype(np.float16).astype(np.float64)
+
+
+def _run(tcbf, prec, w_src, x_src, M, N, K, B, layout="interleaved"):
+    plan = tcbf.Plan(M, N, K, B, prec)
+    wp = plan.pack(tcbf.WEIGHTS, _dev(w_src), layout)
+    xp = plan.pack(tcbf.DATA, _dev(x_src), layout)
+    y = plan.beamform(wp, xp)
+    torch.cuda.synchronize()
+    return plan, wp, xp, y.cpu().numpy()
+
+
+def _check_f16(y, ref, w, x):
+    """y: [B][2][M][N] float32, ref: oracle float64 [B][2][M][N], w,x complex64 sources."""
+    yc = y[:, 0].astype(np.float64) + 1j * y[:, 1]
+    rc = ref[:, 0] + 1j * ref[:, 1]
+    assert np.all(np.isfinite(yc))
+    for b in range(yc.shape[0]):
+        nrm = np.linalg.norm(rc[b])
+        err = np.linalg.norm(yc[b] - rc[b])
+        assert err <= F16_TOL * max(nrm, 1e-30), f"batch {b}: normwise {err / nrm:.3e}"
+    # elementwise diagnostic: |err| <= 8 K u sum_k |w||x| (fp32 accumulation bound)
+    K = w.shape[2]
+    absw = np.abs(w.real.astype(np.float16).astype(np.float64)) + np.abs(w.imag.astype(np.float16).astype(np.float64))
+    absx = np.abs(x.real.astype(np.float16).astype(np.float64)) + np.abs(x.imag.astype(np.float16).astype(np.float64))
+    bound = 8 * K * 2.0 ** -24 * np.matmul(absw, absx) + 1e-30
+    assert np.all(np.abs(yc.real - rc.real) <= bound) and np.all(np.abs(yc.imag - rc.imag) <= bound)
+
+
+# ------------------------------------------------------------------ inputs module twin
+@pytest.mark.parametrize("dist", list(synth.DIST_NAMES))
+def test_device_generator_matches_numpy(dist):
+    B, R, C = 2, 37, 53
+    d = synth.generate_device(dist, 1234, 1, B, R, C).cpu().numpy()
+    h = synth.to_interleaved(synth.generate(dist, 1234, 1, B, R, C))
+    assert np.array_equal(d.view(np.uint32), h.view(np.uint32))
+
+
+# ------------------------------------------------------------------ packing (a1, a2)
+@pytest.mark.parametrize("layout", ["interleaved", "planar"])
+@pytest.mark.parametrize("shape", [(3, 70, 45, 2), (128, 64, 64, 1), (5, 1, 300, 3), (1, 200, 1, 1)])
+def test_pack_f16_bit_exact(tcbf, layout, shape):
+    M, K, N, B = shape
+    w = synth.generate("uniform", 7, 0, B, M, K) * np.float32(3000.0)   # exercise many exponents
+    x = synth.generate("phase_amp", 7, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    lay = 0 if layout == "interleaved" else 1
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout).cpu().numpy().view(np.uint16)
+    xp = plan.pack(tcbf.DATA, _dev(conv(x)), layout).cpu().numpy().view(np.uint16)
+    assert np.array_equal(wp, oracle.pack_f16(conv(w), lay, oracle.WEIGHTS, B, M, K, plan.k_packed))
+    assert np.array_equal(xp, oracle.pack_f16(conv(x), lay, oracle.DATA, B, K, N, plan.k_packed))
+
+
+def test_pack_f16_special_values(tcbf):
+    vals = np.array([0.0, -0.0, 65504.0, 65520.0, 1e6, -1e6, 2.0 ** -25, 2.0 ** -24 * 1.5, np.inf, -np.inf,
+                     1.0 + 2.0 ** -11, 1.0 + 3 * 2.0 ** -11], np.float32)
+    K = vals.size
+    w = np.stack([vals, vals[::-1]], -1).reshape(1, 1, K, 2).astype(np.float32)
+    plan = tcbf.Plan(1, 1, K, 1, "f16")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(w)).cpu().numpy().view(np.uint16)
+    assert np.array_equal(wp, oracle.pack_f16(w, 0, 0, 1, 1, K, plan.k_packed))
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "planar"])
+@pytest.mark.parametrize("shape", [(3, 70, 45, 2), (64, 256, 64, 1), (5, 1, 300, 3), (2, 1000, 33, 2)])
+def test_pack_b1_bit_exact(tcbf, layout, shape):
+    M, K, N, B = shape
+    w = synth.generate("adc", 8, 0, B, M, K)      # exact zeros -> the >= 0 rule
+    x = synth.generate("adc", 8, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    lay = 0 if layout == "interleaved" else 1
+    plan = tcbf.Plan(M, N, K, B, "b1")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout).cpu().numpy().view(np.uint32)
+    xp = plan.pack(tcbf.DATA, _dev(conv(x)), layout).cpu().numpy().view(np.uint32)
+    assert np.array_equal(wp, oracle.pack_b1(conv(w), lay, oracle.WEIGHTS, B, M, K, plan.k_packed))
+    assert np.array_equal(xp, oracle.pack_b1(conv(x), lay, oracle.DATA, B, K, N, plan.k_packed))
+
+
+def test_pack_b1_nan_and_signed_zero(tcbf):
+    vals = np.array([np.nan, -0.0, 0.0, -1e-45, 1e-45, -np.inf, np.inf], np.float32)
+    K = vals.size
+    w = np.stack([vals, vals[::-1]], -1).reshape(1, 1, K, 2)
+    plan = tcbf.Plan(1, 1, K, 1, "b1")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(w)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(wp, oracle.pack_b1(w, 0, 0, 1, 1, K, plan.k_packed))
+
+
+# ------------------------------------------------------------------ fp16 GEMM (a3, a5, a6)
+F16_SHAPES = [
+    (8, 64, 32, 2),        # BASELINE configs[0] (tiny)
+    (200, 300, 100, 3),    # ragged M, N, K; several tiles; N % 4 == 0 -> TMA store
+    (129, 77, 65, 2),      # N % 4 != 0 -> masked-store epilogue; K just over one block
+    (256, 64, 512, 2),     # BN = 64 variant, 8 K blocks
+    (1, 1, 1, 1),          # degenerate
+    (384, 520, 1000, 1),   # many K blocks, ragged
+]
+
+
+@pytest.mark.parametrize("shape", F16_SHAPES)
+def test_f16_beamform_vs_oracle(tcbf, shape):
+    M, N, K, B = shape
+    w = synth.generate("uniform", 21, 0, B, M, K)
+    x = synth.generate("uniform", 21, 1, B, K, N)
+    _, _, _, y = _run(tcbf, "f16", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    ref = oracle.cgemm_f16(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
+    _check_f16(y, ref, w, x)
+
+
+def test_f16_planar_source_same_result(tcbf):
+    M, N, K, B = 130, 96, 70, 2
+    w = synth.generate("phase", 3, 0, B, M, K)
+    x = synth.generate("adc", 3, 1, B, K, N)
+    _, _, _, y0 = _run(tcbf, "f16", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    _, _, _, y1 = _run(tcbf, "f16", synth.to_planar(w), synth.to_planar(x), M, N, K, B, "planar")
+    assert np.array_equal(y0, y1)
+
+
+def test_f16_integer_inputs_exact(tcbf):
+    """Integer entries: every partial sum is exact in fp32, so any accumulation order gives
+    exactly the oracle's value."""
+    rng = np.random.default_rng(4)
+    M, N, K, B = 200, 136, 300, 2
+    w = (rng.integers(-2, 3, (B, M, K)) + 1j * rng.integers(-2, 3, (B, M, K))).astype(np.complex64)
+    x = (rng.integers(-2, 3, (B, K, N)) + 1j * rng.integers(-2, 3, (B, K, N))).astype(np.complex64)
+    _, _, _, y = _run(tcbf, "f16", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    ref = oracle.cgemm_f16(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
+    assert np.array_equal(y.astype(np.float64), ref)
+
+
+def test_f16_identity_weights_exact(tcbf):
+    K, N, B = 150, 200, 2
+    x = synth.generate("adc_scaled", 5, 1, B, K, N)
+    w = np.zeros((B, K, K), np.complex64)
+    w[:, np.arange(K), np.arange(K)] = 1
+    _, _, _, y = _run(tcbf, "f16", synth.to_interleaved(w), synth.to_interleaved(x), K, N, K, B)
+    assert np.array_equal(y[:, 0].astype(np.float64) + 1j * y[:, 1], _rounded(x))
+
+
+def test_f16_plane_wave_steered_beam(tcbf):
+    """Delay-and-sum closed form: the steered beam reaches K|s|."""
+    K, M, N = 256, 121, 64
+    t0 = np.deg2rad(-13.0)
+    th = np.deg2rad(np.linspace(-60, 60, M))
+    m0 = int(np.argmin(np.abs(th - t0)))
+    th[m0] = t0
+    k = np.arange(K)
+    s = synth.generate("uniform", 9, 1, 1, 1, N)[0, 0]
+    x = (np.exp(-1j * np.pi * k * np.sin(t0))[:, None] * s[None, :]).astype(np.complex64)[None]
+    w = np.exp(1j * np.pi * np.outer(np.sin(th), k)).astype(np.complex64)[None]
+    _, _, _, y = _run(tcbf, "f16", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, 1)
+    yc = y[0, 0] + 1j * y[0, 1]
+    assert np.all(np.argmax(np.abs(yc), axis=0) == m0)
+    assert np.allclose(np.abs(yc[m0]), K * np.abs(s), rtol=4e-3)
+
+
+def test_inputs_unmodified(tcbf):
+    M, N, K, B = 64, 64, 64, 1
+    for prec in ("f16", "b1"):
+        w = _dev(synth.to_interleaved(synth.generate("uniform", 1, 0, B, M, K)))
+        x = _dev(synth.to_interleaved(synth.generate("uniform", 1, 1, B, K, N)))
+        w0, x0 = w.clone(), x.clone()
+        plan = tcbf.Plan(M, N, K, B, prec)
+        wp = plan.pack(tcbf.WEIGHTS, w)
+        xp = plan.pack(tcbf.DATA, x)
+        wp0, xp0 = wp.clone(), xp.clone()
+        plan.beamform(wp, xp)
+        torch.cuda.synchronize()
+        assert torch.equal(w, w0) and torch.equal(x, x0) and torch.equal(wp, wp0) and torch.equal(xp, xp0)
+
+
+# ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
+B1_SHAPES = [(8, 64, 32, 2), (70, 45, 300, 3), (64, 64, 256, 1), (1, 1, 1, 1), (130, 200, 1000, 2),
+             (33, 17, 2049, 1), (100, 129, 31, 2)]
+
+
+@pytest.mark.parametrize("shape", B1_SHAPES)
+def test_b1_beamform_bit_exact(tcbf, shape):
+    M, N, K, B = shape
+    w = synth.generate("adc", 31, 0, B, M, K)
+    x = synth.generate("adc", 31, 1, B, K, N)
+    _, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
+    assert np.array_equal(y, ref)
+    refp = oracle.cgemm_b1_packed(wp.cpu().numpy().view(np.uint32), xp.cpu().numpy().view(np.uint32),
+                                  M, N, K, wp.shape[-1], B)
+    assert np.array_equal(y, refp)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4])
+def test_b1_exhaustive(tcbf, K):
+    import itertools
+    V = 4 ** K
+    codes = np.array(list(itertools.product([0, 1], repeat=2 * K)), dtype=np.int64)
+    src = np.stack([np.where(codes[:, :K], 1.0, -1.0), np.where(codes[:, K:], 1.0, -1.0)], -1).astype(np.float32)
+    w = src.reshape(1, V, K, 2)
+    x = np.ascontiguousarray(src.transpose(1, 0, 2)).reshape(1, K, V, 2)
+    _, _, _, y = _run(tcbf, "b1", w, x, V, V, K, 1)
+    assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, V, V, K, 1))
+
+
+def test_b1_random_corpus(tcbf):
+    rng = np.random.default_rng(12)
+    for t in range(40):
+        M, N = int(rng.integers(1, 33)), int(rng.integers(1, 33))
+        K = int(rng.integers(1, 2049))
+        if t % 2 == 0 and K % 32 == 0:
+            K += 1
+        w = rng.standard_normal((1, M, K, 2)).astype(np.float32)
+        x = rng.standard_normal((1, K, N, 2)).astype(np.float32)
+        _, _, _, y = _run(tcbf, "b1", w, x, M, N, K, 1)
+        assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, M, N, K, 1)), (M, N, K)
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+def _full_size(tcbf, prec, M, N, K, B, wdist, xdist, seed, batches, rows):
+    plan = tcbf.Plan(M, N, K, B, prec)
+    wsrc = synth.generate_device(wdist, seed, 0, B, M, K)
+    wp = plan.pack(tcbf.WEIGHTS, wsrc)
+    del wsrc
+    xsrc = synth.generate_device(xdist, seed, 1, B, K, N)
+    xp = plan.pack(tcbf.DATA, xsrc)
+    del xsrc
+    y = plan.beamform(wp, xp)
+    torch.cuda.synchronize()
+    nr = len(rows)
+    for b in batches:
+        w = synth.generate(wdist, seed, 0, B, M, K, b_sel=[b], r_sel=rows)   # only the sampled beams
+        x = synth.generate(xdist, seed, 1, B, K, N, b_sel=[b])
+        got = y[b][:, rows].cpu().numpy()[None]
+        if prec == "b1":
+            ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, nr, N, K, 1)
+            assert np.array_equal(got, ref)
+        else:
+            ref = oracle.cgemm_f16(synth.to_interleaved(w), synth.to_interleaved(x), 0, nr, N, K, 1)
+            _check_f16(got, ref, w, x)
+    return y
+
+
+def test_full_size_radio_f16_sampled(tcbf):
+    """BASELINE configs[1]: M=1024, K=256, N=1024, batch=256, launch as bench.py times it."""
+    _full_size(tcbf, "f16", 1024, 1024, 256, 256, "phase", "adc", synth.SEED_BASE + 1,
+               batches=[0, 131, 255], rows=[0, 1, 127, 128, 511, 1000, 1023])
+
+
+def test_full_size_radio_b1_sampled(tcbf):
+    """BASELINE configs[2]: M=1024, K=512, N=4096, batch=256."""
+    _full_size(tcbf, "b1", 1024, 4096, 512, 256, "phase", "adc", synth.SEED_BASE + 2,
+               batches=[0, 200, 255], rows=[0, 63, 64, 777, 1023])
+
+
+def test_full_size_ultrasound_f16_sampled(tcbf):
+    """BASELINE configs[3]: M=65536, K=8192, N=256, batch=8 (17 GB of packed weights)."""
+    _full_size(tcbf, "f16", 65536, 256, 8192, 8, "phase_amp", "adc_scaled", synth.SEED_BASE + 3,
+               batches=[0, 7], rows=[0, 4097, 65535])
