@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Tensor-Core Beamformer hot path (BASELINE.json metric:
+"beamforming TeraOps/s (fp16 and 1-bit) at 1/2/4/8 B200 vs roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config radio_f16] [--impl tcbf|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+A step = one pass of the hot path over one batch of synthetic data resident in HBM:
+tcbf_pack(DATA) (fp32 -> packed operand, §8 a1/a2) + tcbf_beamform (§8 a3-a6).  The
+weights are packed once before timing (the model matrix is prepared once;
+PAPER.md:48: weights constant over a period).  Useful ops = 8*B*M*N*K.
+Multi-GPU: weak scaling, every rank beamforms its own `batch` channels (global batch =
+N x batch), no data-path collective; time = max over ranks of CUDA-event time.
+Default workload = BASELINE configs[1] (radio astronomy fp16, LOFAR-shaped).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 2 ** 20
+
+
+def _cfg(prec, M, N, K, B, wd, xd, idx, desc):
+    return dict(prec=prec, M=M, N=N, K=K, B=B, wd=wd, xd=xd, idx=idx, desc=desc)
+
+
+CONFIGS = {
+    "tiny": _cfg("f16", 8, 64, 32, 2, "uniform", "uniform", 0,
+                 "tiny fp16: M=8 beams, K=32 receivers, N=64 samples, batch=2"),
+    "radio_f16": _cfg("f16", 1024, 1024, 256, 256, "phase", "adc", 1,
+                      "radio astronomy fp16: M=1024 beams, K=256 stations, N=1024 samples, batch=256 channels"),
+    "radio_b1": _cfg("b1", 1024, 4096, 512, 256, "phase", "adc", 2,
+                     "radio astronomy 1-bit: M=1024 beams, K=512 stations, N=4096 samples, batch=256 channels"),
+    "ultrasound_f16": _cfg("f16", 65536, 256, 8192, 8, "phase_amp", "adc_scaled", 3,
+                           "computational ultrasound fp16: M=65536 pixels, K=8192, N=256 frames, batch=8"),
+    # Fig. 3 extra rows
+    "fig3_f16_small": _cfg("f16", 1024, 1024, 64, 256, "uniform", "uniform", 4, "fp16 small 256x1024x1024x64"),
+    "fig3_b1_small": _cfg("b1", 1024, 1024, 256, 256, "uniform", "uniform", 4, "int1 small 256x1024x1024x256"),
+}
+for _n in (1024, 2048, 4096, 8192, 16384):
+    CONFIGS[f"square_f16_{_n}"] = _cfg("f16", _n, _n, _n, 1, "uniform", "uniform", 4, f"square fp16 M=N=K={_n}")
+    CONFIGS[f"square_b1_{_n}"] = _cfg("b1", _n, _n, _n, 1, "uniform", "uniform", 4, f"square 1-bit M=N=K={_n}")
+    CONFIGS[f"m32_f16_{_n}"] = _cfg("f16", 32, _n, _n, 1, "uniform", "uniform", 4, f"M=32 fp16 N=K={_n}")
+    CONFIGS[f"m32_b1_{_n}"] = _cfg("b1", 32, _n, _n, 1, "uniform", "uniform", 4, f"M=32 1-bit N=K={_n}")
+
+
+def useful_ops(c):
+    return 8.0 * c["M"] * c["N"] * c["K"] * c["B"]
+
+
+def gemm_bytes(c):
+    """Algorithmic bytes of one beamform launch (PAPER.md:319 'theoretical amount
+    of bytes'): logical inputs read once, output written once."""
+    B, M, N, K = c["B"], c["M"], c["N"], c["K"]
+    if c["prec"] == "f16":
+        return B * (4 * M * K + 4 * K * N + 8 * M * N)
+    return B * ((M * K + K * N) / 4.0 + 8 * M * N)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm=float(d["hbm_gbs"]), bf16=float(d["bf16_tflops"]),
+                    bf16_sus=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), src="measured")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+def roofline_for(c, gemm_ms, peaks, long_step):
+    """Dominant kernel = the beamform GEMM.  f16: tensor peak = measured bf16 peak x 1 (same
+    nominal rate); b1 (popc on CUDA cores): bound 'alu' against the derived POPC peak."""
+    ops = useful_ops(c)
+    byts = gemm_bytes(c)
+    bw = peaks["hbm"]
+    if c["prec"] == "f16":
+        tflops = peaks["bf16_sus"] if long_step else peaks["bf16"]
+        ridge = tflops * 1e12 / (bw * 1e9)
+        if ops / byts < ridge:
+            ach = byts / (gemm_ms * 1e-3) / 1e9
+            return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
+                        peak_src=peaks["src"])
+        ach = ops / (gemm_ms * 1e-3) / 1e12
+        return dict(bound="tensor", achieved=round(ach, 1), peak=tflops, unit="TFLOP/s", frac=round(ach / tflops, 4),
+                    peak_src=peaks["src"] + (" sustained" if long_step else " burst"))
+    # 1-bit popc kernel: 4 POPC per complex 32-bit word quadruple -> peak useful ops =
+    # popc_per_clk_per_sm * 148 SMs * clk * 32 bits * 2 (ops per MAC); 16 POPC/clk/SM
+    alu_peak = 16 * 148 * 1.965e9 * 32 * 2 / 1e12
+    ach = ops / (gemm_ms * 1e-3) / 1e12
+    return dict(bound="alu", achieved=round(ach, 1), peak=round(alu_peak, 1), unit="TOP/s",
+                frac=round(ach / alu_peak, 4), peak_src="derived (16 POPC/clk/SM x 148 x 1965 MHz)")
+
+
+def traffic_for(c_name, variant):
+    """dram bytes per launch from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(c_name)
+        if e and e.get("variant") == variant:
+            return e.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        active = [n for bit, n in self.NAMES.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": active,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def oracle_sample(c, seconds, rank_b0=0, budget_rows=None):
+    """Time the oracle (as it stands) on a bounded sample of the workload: the first `rows`
+    beams of batch entry 0 (all N samples, all K receivers).  Returns (ops/s, rows, sec)."""
+    import numpy as np
+    import oracle
+    import synth
+    seed = synth.SEED_BASE + c["idx"]
+    M, N, K, B = c["M"], c["N"], c["K"], c["B"]
+    x = synth.to_interleaved(synth.generate(c["xd"], seed, 1, B, K, N, b_sel=[rank_b0]))
+
+    def run(rows):
+        w = synth.to_interleaved(synth.generate(c["wd"], seed, 0, B, M, K, b_sel=[rank_b0], r_sel=slice(0, rows)))
+        t0 = time.perf_counter()
+        if c["prec"] == "f16":
+            oracle.cgemm_f16(w, x, 0, rows, N, K, 1)
+        else:
+            oracle.cgemm_b1(w, x, 0, rows, N, K, 1)
+        return time.perf_counter() - t0
+
+    rows = budget_rows or min(M, 4)
+    t = run(rows)
+    if budget_rows is None:
+        while t < seconds * 0.25 and rows < M:
+            rows = min(M, max(rows + 1, int(rows * min(8.0, seconds / max(t, 1e-4)))))
+            t = run(rows)
+    ops = 8.0 * rows * N * K
+    return ops / t, rows, t
+
+
+def cpu_baseline(c, seconds=12.0):
+    rate, rows, t = oracle_sample(c, seconds)
+    return {"value": round(rate / 1e12, 6), "unit": "TeraOps/s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"oracle (C, fp64/int64 triple loop, OpenMP {os.cpu_count()} threads) on beams 0..{rows - 1} "
+                      f"of batch entry 0 (all N={c['N']}, K={c['K']}); {t:.1f} s"}
+
+
+def run_reference(args, c):
+    """--impl reference: the oracle as it stands is this tier's reference arm."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    budget = max(0.05, min(0.5, 150.0 / max(1, args.steps + args.warmup)))
+    rate, rows, t = oracle_sample(c, budget * 4)
+    # rows chosen so one step ~ budget seconds
+    rows = max(1, min(c["M"], int(rows * budget / max(t, 1e-6))))
+    for _ in range(args.warmup):
+        oracle_sample(c, 0, budget_rows=rows)
+    times = []
+    for s in range(args.steps):
+        r, _, tt = oracle_sample(c, 0, budget_rows=rows)
+        times.append(tt)
+    tot = sum(times)
+    ops = 8.0 * rows * c["N"] * c["K"] * args.steps
+    val = ops / tot / 1e12
+    sample = (f"each step: oracle on beams 0..{rows - 1} of batch entry 0 (N={c['N']}, K={c['K']}), "
+              f"{os.cpu_count()} OpenMP threads")
+    line = {"metric": "beamforming TeraOps/s (fp16 and 1-bit) at 1/2/4/8 B200 vs roofline", "impl": "reference",
+            "value": round(val, 6), "unit": "TeraOps/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if c["prec"] == "f16" else "int64",
+            "data": "synthetic (seeded counter-based generator, synth/)",
+            "config": {"workload": args.config, "desc": c["desc"], "M": c["M"], "N": c["N"], "K": c["K"],
+                       "batch_per_gpu": c["B"]},
+            "cpu_baseline": {"value": round(val, 6), "unit": "TeraOps/s", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(val, 6), "unit": "TeraOps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_tcbf(args, c):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_03269_b200 as tcbf
+    import synth
+    from paper_2505_03269_b200.shard import max_over_ranks, weak_shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    sh = weak_shard(c["B"], rank)
+    M, N, K, B = c["M"], c["N"], c["K"], c["B"]
+    seed = synth.SEED_BASE + c["idx"]
+    plan = tcbf.Plan(M, N, K, B, c["prec"])
+
+    wsrc = synth.generate_device(c["wd"], seed, 0, B, M, K, device=dev, b0=sh.b0)
+    wp = plan.pack(tcbf.WEIGHTS, wsrc)
+    del wsrc
+    xsrc = synth.generate_device(c["xd"], seed, 1, B, K, N, device=dev, b0=sh.b0)
+    xp = plan.alloc_packed(tcbf.DATA, dev)
+    out = plan.alloc_output(dev)
+    torch.cuda.synchronize()
+
+    working = xsrc.numel() * 4 + plan.x_bytes + plan.w_bytes + plan.out_bytes
+    flush = working < 4 * L2_BYTES
+    flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
+        plan.beamform(wp, xp, out, stream=stream)
+
+    for _ in range(args.warmup):
+        if flush:
+            flush_buf.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        if flush:
+            flush_buf.fill_(float(i))   # evict L2 between timed steps (not inside the timed spans)
+        ev[i][0].record(stream)
+        plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
+        ev[i][1].record(stream)
+        plan.beamform(wp, xp, out, stream=stream)
+        ev[i][2].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler.stop()
+    if flush:
+        total_ms = sum(e[0].elapsed_time(e[2]) for e in ev)
+    else:
+        total_ms = ev[0][0].elapsed_time(ev[-1][2])
+    gemm_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    pack_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    ms_step = max_over_ranks(total_ms / args.steps, dev)
+    gemm_ms_max = max_over_ranks(gemm_ms, dev)
+    value = world * useful_ops(c) / (ms_step * 1e-3) / 1e12
+
+    # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
+    x_host = xsrc.cpu().pin_memory()
+    out_host = torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory()
+    e2e_steps = max(1, min(args.steps, int(os.environ.get("TCBF_E2E_STEPS", "5"))))
+    plan.beamform_host(wp, x_host, out_host)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.beamform_host(wp, x_host, out_host)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_s = max_over_ranks(e2e_s, dev)
+    e2e_val = world * useful_ops(c) / e2e_s / 1e12
+
+    peaks = load_peaks()
+    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0))
+    roof["traffic"] = traffic_for(args.config, plan.variant)
+    roof["kernel"] = plan.variant
+    roof["kernel_ms"] = round(gemm_ms_max, 4)
+    roof["algorithmic_bytes_per_launch"] = gemm_bytes(c)
+    roof["useful_ops_per_launch"] = useful_ops(c)
+
+    line = {
+        "metric": "beamforming TeraOps/s (fp16 and 1-bit) at 1/2/4/8 B200 vs roofline",
+        "value": round(value, 2), "unit": "TeraOps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": c["prec"], "data": "synthetic (seeded counter-based generator, synth/)",
+        "config": {"workload": args.config, "desc": c["desc"], "M": M, "N": N, "K": K, "batch_per_gpu": B,
+                   "global_batch": B * world, "precision": c["prec"],
+                   "step": "tcbf_pack(data) + tcbf_beamform; weights packed once",
+                   "l2": ("flushed between steps (256 MiB write)" if flush else
+                          f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
+                   "parallelism": f"batch-sharded x{world}, no data-path collective",
+                   "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4)},
+        "roofline": roof,
+        "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s", "h2d_bytes_per_step": int(x_host.numel() * 4),
+                "d2h_bytes_per_step": int(plan.out_bytes), "api": "tcbf_beamform_host (pinned host buffers)",
+                "steps": e2e_steps},
+        "gpu_launches": 2 * args.steps,
+        "clocks": sampler.summary(),
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(c)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="radio_f16", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="tcbf", choices=["tcbf", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, c)
+    return run_tcbf(args, c)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
