@@ -1,0 +1,350 @@
+// gemm_b1_tc.cu -- 1-bit-mode complex beamformer GEMM on the sm_100a tensor cores (kind::i8).
+//
+// The paper's 1-bit tensor-core path (b1 mma with XOR/AND + popc) does not
+// exist natively on sm_100a: ptxas lowers `mma.sync ... .b1 ... .popc` to 8 legacy
+// IMMA.16832.U8 + LOP3 masks per m16n8k256 (cuobjdump -sass; profiles/).  This kernel keeps
+// HBM traffic at one bit per component and feeds the 5th-generation tensor cores instead:
+//
+//   * the packed words are expanded IN SHARED MEMORY to unsigned bytes u in {0, 1} by bit-plane
+//     masking, byte i of plane j = bit (8i + j) of the word: (w >> j) & 0x01010101.  This is a
+//     fixed permutation of the 32 K-elements of a word, applied identically to both operands,
+//     so every dot product is unchanged;
+//   * tcgen05.mma.kind::i8 (unsigned, int32 accumulate in TMEM) then computes AND-popcounts
+//     P(A & B) = sum_k u_a u_b exactly (PAPER.md:265-270 AND form);
+//   * the complex +-1 result follows from the single-AND identities (reading R1b),
+//     with a = 2u - 1 and |X| the popcount of a row/column:
+//         acc_r = P(A_r & B_r) + P(A_i & ~B_i)          acc_i = P(A_r & B_i) + P(A_i & B_r)
+//         Re = 4 acc_r - 2|A_r| - 2|A_i| - 2|B_r| + 2|B_i|
+//         Im = 4 acc_i - 2(|A_r| + |A_i| + |B_r| + |B_i|) + 2K
+//     ~B_i is formed during expansion, the paper's "Im(b) = -Im(b) in local registers"
+//     (PAPER.md:154-159).  Padding bits are 0 in A, so the 1s of ~B_i in the padding never
+//     contribute; no K_pad term is needed.
+//
+// Roles (persistent CTA per SM, 416 threads):
+//   warp 0      TMEM allocator + single-thread MMA issuer (4 MMAs per K=32 step)
+//   warps 1-4   epilogue: row/column popcounts, tcgen05.ld, correction, TMA store of int32
+//   warps 5-8   expanders for A_r, A_i (one weight row per thread)
+//   warps 9-12  expanders for B_r, B_i, ~B_i (one data column per thread)
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tcbf {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int KB_WORDS = 4;            // 128 bits per K block -> 128 expanded bytes per row
+constexpr int TILE_BYTES = 128 * 128;  // one expanded operand tile (rows x 128 B)
+constexpr int STAGES = 2;
+constexpr int STAGE_BYTES = 5 * TILE_BYTES;  // A_r, A_i, B_r, B_i, ~B_i
+constexpr int EPI_BYTES = 4 * 2 * 4096;
+constexpr int COLSUM_BYTES = 2 * 2 * BN * 4;
+constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES + COLSUM_BYTES;
+constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+constexpr int NUM_THREADS = 13 * 32;
+constexpr int NUM_EXPANDERS = 256;
+constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (acc_r, acc_i) x 128 columns
+static_assert(SMEM_BYTES <= 232448, "smem budget");
+
+__device__ __forceinline__ void expand_word(uint8_t* row_base, int row, int q, uint32_t w) {
+  // word q of the K block -> chunks 2q (planes 0-3) and 2q+1 (planes 4-7), 128-byte swizzle
+  const uint32_t m = 0x01010101u;
+  uint4 c0 = make_uint4(w & m, (w >> 1) & m, (w >> 2) & m, (w >> 3) & m);
+  uint4 c1 = make_uint4((w >> 4) & m, (w >> 5) & m, (w >> 6) & m, (w >> 7) & m);
+  const int sw = row & 7;
+  *reinterpret_cast<uint4*>(row_base + (((2 * q) ^ sw) << 4)) = c0;
+  *reinterpret_cast<uint4*>(row_base + (((2 * q + 1) ^ sw) << 4)) = c1;
+}
+
+// expands w and its complement (planes of ~w are planes of w xor 0x01010101)
+__device__ __forceinline__ void expand_word_pair(uint8_t* base, uint8_t* base_c, int row, int q, uint32_t w) {
+  const uint32_t m = 0x01010101u;
+  uint4 c0 = make_uint4(w & m, (w >> 1) & m, (w >> 2) & m, (w >> 3) & m);
+  uint4 c1 = make_uint4((w >> 4) & m, (w >> 5) & m, (w >> 6) & m, (w >> 7) & m);
+  const int sw = row & 7;
+  const int p0 = ((2 * q) ^ sw) << 4, p1 = ((2 * q + 1) ^ sw) << 4;
+  *reinterpret_cast<uint4*>(base + p0) = c0;
+  *reinterpret_cast<uint4*>(base + p1) = c1;
+  *reinterpret_cast<uint4*>(base_c + p0) = make_uint4(c0.x ^ m, c0.y ^ m, c0.z ^ m, c0.w ^ m);
+  *reinterpret_cast<uint4*>(base_c + p1) = make_uint4(c1.x ^ m, c1.y ^ m, c1.z ^ m, c1.w ^ m);
+}
+
+__device__ __forceinline__ int popc_row(const uint32_t* __restrict__ row, int Kw) {
+  int s = 0;
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  for (int i = 0; i < Kw / 4; ++i) {
+    uint4 v = __ldg(r4 + i);
+    s += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  return s;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool TMA_STORE>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cgemm_b1_tc_kernel(const __grid_constant__ CUtensorMap tmC, GemmB1Args p, int tiles_m, int tiles_n,
+                       int num_tiles) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* epi_base = smem + STAGES * STAGE_BYTES;
+  int* colsum = reinterpret_cast<int*>(epi_base + EPI_BYTES);  // [2 buf][2 plane][BN]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_kb = p.Kw / KB_WORDS;
+  const int tiles_per_batch = tiles_m * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], NUM_EXPANDERS);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+    if (TMA_STORE) tma_prefetch_desc(&tmC);
+  }
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // kind::i8, unsigned A and B, int32 D, K-major, M = 128, N = BN
+      constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)(BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(&tempty_bar[abuf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_re = tmem_base + abuf * 2 * BN;
+        const uint32_t d_im = d_re + BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * STAGE_BYTES;
+          uint8_t* sAr = st;
+          uint8_t* sAi = st + TILE_BYTES;
+          uint8_t* sBr = st + 2 * TILE_BYTES;
+          uint8_t* sBi = st + 3 * TILE_BYTES;
+          uint8_t* sBc = st + 4 * TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // K = 32 bytes per MMA
+            const uint32_t off = kk * 32;
+            const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
+            const uint64_t br = smem_desc_k128(sBr, off), bi = smem_desc_k128(sBi, off);
+            const uint64_t bc = smem_desc_k128(sBc, off);
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            mma_i8_ss(d_re, ar, br, IDESC, acc);  // P(A_r & B_r)
+            mma_i8_ss(d_re, ai, bc, IDESC, 1u);   // P(A_i & ~B_i)
+            mma_i8_ss(d_im, ar, bi, IDESC, acc);  // P(A_r & B_i)
+            mma_i8_ss(d_im, ai, br, IDESC, 1u);   // P(A_i & B_r)
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull_bar[abuf]);
+      }
+    }
+  } else if (warp <= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int ew = warp - 1;
+    const int te = ew * 32 + lane;  // column handled for the column popcounts
+    uint8_t* stg = epi_base + ew * 8192;
+    int sbuf = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int b = t / tiles_per_batch;
+      const int r = t - b * tiles_per_batch;
+      const int m0 = (r / tiles_n) * BM;
+      const int n0 = (r % tiles_n) * BN;
+      const int cb = it & 1;
+      // popcounts |B_r|, |B_i| of this tile's columns and |A_r|, |A_i| of this thread's row
+      {
+        const int n = n0 + te;
+        int pr = 0, pi = 0;
+        if (n < p.N) {
+          pr = popc_row(p.x + ((size_t)(2 * b) * p.N + n) * p.Kw, p.Kw);
+          pi = popc_row(p.x + ((size_t)(2 * b + 1) * p.N + n) * p.Kw, p.Kw);
+        }
+        colsum[(cb * 2 + 0) * BN + te] = pr;
+        colsum[(cb * 2 + 1) * BN + te] = pi;
+      }
+      const int m = m0 + q * 32 + lane;
+      int ra = 0;
+      if (m < p.M) {
+        ra = popc_row(p.w + ((size_t)(2 * b) * p.M + m) * p.Kw, p.Kw) +
+             popc_row(p.w + ((size_t)(2 * b + 1) * p.M + m) * p.Kw, p.Kw);
+      }
+      named_bar_sync(1, 128);
+      const int* csr = colsum + (cb * 2 + 0) * BN;
+      const int* csi = colsum + (cb * 2 + 1) * BN;
+
+      const int abuf = it & 1;
+      mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
+      tc_fence_after();
+      constexpr int CHUNKS = BN / 32;
+#pragma unroll 1
+      for (int ch = 0; ch < 2 * CHUNKS; ++ch) {
+        const int part = ch / CHUNKS;
+        const int c = ch % CHUNKS;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN + part * BN + c * 32, v);
+        tmem_wait_ld();
+        if (ch == 2 * CHUNKS - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int cr = csr[c * 32 + j], ci = csi[c * 32 + j];
+          const int acc = (int)v[j];
+          const int val = part == 0 ? 4 * acc - 2 * ra - 2 * cr + 2 * ci
+                                    : 4 * acc - 2 * (ra + cr + ci) + 2 * p.K;
+          v[j] = (uint32_t)val;
+        }
+        if constexpr (TMA_STORE) {
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+          uint8_t* buf = stg + sbuf * 4096;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pos = j ^ (lane & 7);
+            *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
+                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
+            bulk_commit_group();
+          }
+          sbuf ^= 1;
+        } else {
+          if (m < p.M) {
+            int32_t* row = p.out + ((size_t)(2 * b + part) * p.M + m) * (size_t)p.N;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = n0 + c * 32 + j;
+              if (n < p.N) row[n] = (int32_t)v[j];
+            }
+          }
+        }
+      }
+    }
+    if constexpr (TMA_STORE) {
+      if (lane == 0) bulk_wait_group<0>();
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ expanders
+    const int e = threadIdx.x - 5 * 32;  // 0..255
+    const bool a_side = e < 128;
+    const int row = a_side ? e : e - 128;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int b = t / tiles_per_batch;
+      const int r = t - b * tiles_per_batch;
+      const int m0 = (r / tiles_n) * BM;
+      const int n0 = (r % tiles_n) * BN;
+      const uint4* src_r;
+      const uint4* src_i;
+      bool valid;
+      if (a_side) {
+        valid = (m0 + row) < p.M;
+        src_r = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b) * p.M + m0 + row) * p.Kw);
+        src_i = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b + 1) * p.M + m0 + row) * p.Kw);
+      } else {
+        valid = (n0 + row) < p.N;
+        src_r = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b) * p.N + n0 + row) * p.Kw);
+        src_i = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b + 1) * p.N + n0 + row) * p.Kw);
+      }
+      const uint4 zero = make_uint4(0, 0, 0, 0);
+      uint4 nr = valid ? __ldg(src_r) : zero;
+      uint4 ni = valid ? __ldg(src_i) : zero;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        const uint4 wr = nr, wi = ni;
+        if (kb + 1 < num_kb) {
+          nr = valid ? __ldg(src_r + kb + 1) : zero;
+          ni = valid ? __ldg(src_i + kb + 1) : zero;
+        }
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* st = smem + stage * STAGE_BYTES;
+        if (a_side) {
+          uint8_t* ar = st + row * 128;
+          uint8_t* ai = st + TILE_BYTES + row * 128;
+          expand_word(ar, row, 0, wr.x); expand_word(ar, row, 1, wr.y);
+          expand_word(ar, row, 2, wr.z); expand_word(ar, row, 3, wr.w);
+          expand_word(ai, row, 0, wi.x); expand_word(ai, row, 1, wi.y);
+          expand_word(ai, row, 2, wi.z); expand_word(ai, row, 3, wi.w);
+        } else {
+          uint8_t* br = st + 2 * TILE_BYTES + row * 128;
+          uint8_t* bi = st + 3 * TILE_BYTES + row * 128;
+          uint8_t* bc = st + 4 * TILE_BYTES + row * 128;
+          expand_word(br, row, 0, wr.x); expand_word(br, row, 1, wr.y);
+          expand_word(br, row, 2, wr.z); expand_word(br, row, 3, wr.w);
+          expand_word_pair(bi, bc, row, 0, wi.x); expand_word_pair(bi, bc, row, 1, wi.y);
+          expand_word_pair(bi, bc, row, 2, wi.z); expand_word_pair(bi, bc, row, 3, wi.w);
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
+        mbar_arrive(&full_bar[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <bool TMA_STORE>
+cudaError_t launch_tc(const CUtensorMap& tmC, const GemmB1Args& a, int num_sms, cudaStream_t stream) {
+  auto kern = cgemm_b1_tc_kernel<TMA_STORE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const long long nt = (long long)tiles_m * tiles_n * a.B;
+  if (nt > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int grid = (int)(nt < num_sms ? nt : num_sms);
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmC, a, tiles_m, tiles_n, (int)nt);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
+                              cudaStream_t stream) {
+  return tma_store ? launch_tc<true>(tmC, args, num_sms, stream) : launch_tc<false>(tmC, args, num_sms, stream);
+}
+
+}  // namespace tcbf

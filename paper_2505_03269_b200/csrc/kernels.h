@@ -24,6 +24,8 @@ struct GemmB1Args {
   int M, N, K, Kw, B;
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
+cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
+                              cudaStream_t stream);
 
 // pack kernels (pack.cu)
 cudaError_t launch_pack_f16(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,

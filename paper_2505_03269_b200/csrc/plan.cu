@@ -153,6 +153,8 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     int v = atoi(env);
     if (v == 64 || v == 128) p->block_n = v;
   }
+  p->b1_tc = 1;
+  if (const char* env = getenv("TCBF_B1_KERNEL")) p->b1_tc = strcmp(env, "popc") == 0 ? 0 : 1;
   *plan = p;
   return TCBF_OK;
 }
@@ -177,7 +179,10 @@ tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes) {
 
 const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (!plan) return "none";
-  if (plan->prec == TCBF_PREC_B1) return "b1_popc_xor_64x64";
+  if (plan->prec == TCBF_PREC_B1) {
+    if (!plan->b1_tc) return "b1_popc_xor_64x64";
+    return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
+  }
   if (plan->N % 4 != 0) return plan->block_n == 64 ? "f16_tcgen05_128x64_stg" : "f16_tcgen05_128x128_stg";
   return plan->block_n == 64 ? "f16_tcgen05_128x64_tma" : "f16_tcgen05_128x128_tma";
 }
@@ -248,7 +253,19 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.x = static_cast<const uint32_t*>(x_packed);
     a.out = static_cast<int32_t*>(out);
     a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
-    e = tcbf::launch_gemm_b1_popc(a, st);
+    if (plan->b1_tc) {
+      const bool tma_store = (plan->N % 4) == 0;
+      CUtensorMap tc;
+      memset(&tc, 0, sizeof(tc));
+      if (tma_store) {
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (s != TCBF_OK) return s;
+      }
+      e = tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
+    } else {
+      e = tcbf::launch_gemm_b1_popc(a, st);
+    }
   }
   if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
   g_launches = 1;

@@ -12,6 +12,7 @@ struct tcbf_plan_s {
   int device;
   int num_sms;
   int block_n;  // fp16 GEMM tile width
+  int b1_tc;    // 1 = tensor-core (kind::i8) 1-bit kernel, 0 = CUDA-core popc kernel
   size_t w_bytes, x_bytes, out_bytes;
 };
 

@@ -198,12 +198,19 @@ def test_inputs_unmodified(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
+@pytest.fixture(params=["tc", "popc"])
+def b1_kernel(request, monkeypatch):
+    """Both 1-bit kernels: tcgen05 kind::i8 (default) and the CUDA-core XOR/popc kernel."""
+    monkeypatch.setenv("TCBF_B1_KERNEL", request.param)
+    return request.param
+
+
 B1_SHAPES = [(8, 64, 32, 2), (70, 45, 300, 3), (64, 64, 256, 1), (1, 1, 1, 1), (130, 200, 1000, 2),
              (33, 17, 2049, 1), (100, 129, 31, 2)]
 
 
 @pytest.mark.parametrize("shape", B1_SHAPES)
-def test_b1_beamform_bit_exact(tcbf, shape):
+def test_b1_beamform_bit_exact(tcbf, shape, b1_kernel):
     M, N, K, B = shape
     w = synth.generate("adc", 31, 0, B, M, K)
     x = synth.generate("adc", 31, 1, B, K, N)
@@ -216,7 +223,7 @@ def test_b1_beamform_bit_exact(tcbf, shape):
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4])
-def test_b1_exhaustive(tcbf, K):
+def test_b1_exhaustive(tcbf, K, b1_kernel):
     import itertools
     V = 4 ** K
     codes = np.array(list(itertools.product([0, 1], repeat=2 * K)), dtype=np.int64)
@@ -227,7 +234,7 @@ def test_b1_exhaustive(tcbf, K):
     assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, V, V, K, 1))
 
 
-def test_b1_random_corpus(tcbf):
+def test_b1_random_corpus(tcbf, b1_kernel):
     rng = np.random.default_rng(12)
     for t in range(40):
         M, N = int(rng.integers(1, 33)), int(rng.integers(1, 33))
@@ -271,7 +278,7 @@ def test_full_size_radio_f16_sampled(tcbf):
                batches=[0, 131, 255], rows=[0, 1, 127, 128, 511, 1000, 1023])
 
 
-def test_full_size_radio_b1_sampled(tcbf):
+def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
     """BASELINE configs[2]: M=1024, K=512, N=4096, batch=256."""
     _full_size(tcbf, "b1", 1024, 4096, 512, 256, "phase", "adc", synth.SEED_BASE + 2,
                batches=[0, 200, 255], rows=[0, 63, 64, 777, 1023])
