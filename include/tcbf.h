@@ -26,8 +26,9 @@
  * Layouts (row-major, innermost last):
  *   fp32 sources    weights  W: interleaved [B][M][K] float2 | planar [B][2][M][K]
  *                   data     X: interleaved [B][K][N] float2 | planar [B][2][K][N]
- *   packed F16      weights  [B][2][M][Kp] fp16,  data (transposed) [B][2][N][Kp] fp16
- *                   Kp = round_up(K, 64); K padding is 0.0.
+ *   packed F16      weights  [B][2][M][Kp] fp16 (K-major), Kp = round_up(K, 64), K padding 0.0;
+ *                   data     [B][2][K][Np] fp16 (N-contiguous, consumed MN-major by the
+ *                   tensor cores, no transpose), Np = round_up(N, 8), N padding 0.0.
  *   packed B1       weights  [B][2][M][Kp] uint32, data (transposed) [B][2][N][Kp] uint32
  *                   Kp = round_up(ceil(K/32), 8) words; bit k%32 of word k/32 is
  *                   element k (LSB-first, reading R3); padding bits are 0.
@@ -65,7 +66,8 @@ typedef struct tcbf_plan_s tcbf_plan;
 
 /* Host-only layout arithmetic (no device needed).  Any output pointer may be NULL.
  * w_bytes / x_bytes: packed weight / data buffer sizes; out_bytes: output size;
- * k_packed: Kp (fp16 elements for F16, uint32 words for B1).
+ * k_packed: Kp (fp16 elements for F16, uint32 words for B1).  F16 packed data rows are
+ * Np = round_up(N, 8) elements long (see the layout table above).
  * Errors: INVALID_ARG if M, N, K, batch < 1, if a size overflows size_t, or if
  * B1 and K >= 2^30 (|Re|,|Im| <= 2K must fit int32). */
 tcbf_status tcbf_layout_sizes(int64_t M, int64_t N, int64_t K, int64_t batch,
@@ -92,7 +94,8 @@ tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes);
  *   F16: fp32 -> fp16 round-to-nearest-even (IEEE: overflow -> inf, NaN stays NaN).
  *   B1:  sign quantisation, bit = (value >= 0).
  * src: fp32 source in `layout` (see top); dst: packed buffer of tcbf_packed_bytes().
- * The DATA operand is transposed to N-major/K-contiguous.  src must be 8-byte
+ * B1 DATA is transposed to [B][2][N][Kp] (bits run along K); F16 DATA keeps the
+ * [K][N] order (the GEMM reads it MN-major).  src must be 8-byte
  * aligned (interleaved) or 4-byte aligned (planar); dst 16-byte aligned.
  * dst and src must not overlap. */
 tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src,

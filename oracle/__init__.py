@@ -128,12 +128,12 @@ def cgemm_b1_packed(wp: np.ndarray, xp: np.ndarray, M: int, N: int, K: int, Kw: 
 
 
 def pack_f16(src: np.ndarray, layout: int, operand: int, B: int, R: int, C: int,
-             K16: int) -> np.ndarray:
-    """uint16 fp16 bit patterns, [B][2][rows][K16] (rows = M or N)."""
+             Cp: int) -> np.ndarray:
+    """uint16 fp16 bit patterns, [B][2][R][Cp]: weights (R=M, C=K, Cp=K16) or data
+    (R=K, C=N, Cp=Np) -- both keep their row order, zero column padding."""
     src = _src(src)
-    rows = R if operand == WEIGHTS else C
-    out = np.empty((B, 2, rows, K16), dtype=np.uint16)
-    rc = lib().oracle_pack_f16(_ptr(src), layout, operand, B, R, C, K16, _ptr(out))
+    out = np.empty((B, 2, R, Cp), dtype=np.uint16)
+    rc = lib().oracle_pack_f16(_ptr(src), layout, operand, B, R, C, Cp, _ptr(out))
     if rc != 0:
         raise ValueError(f"oracle_pack_f16 rc={rc}")
     return out

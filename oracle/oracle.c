@@ -20,7 +20,7 @@
  *   sources (fp32):   weights W [B][M][K], data X [B][K][N]
  *     layout 0 = interleaved float2 (re, im adjacent)
  *     layout 1 = planar [B][2][rows][cols] (re plane then im plane)
- *   packed f16:  weights [B][2][M][K16], data transposed [B][2][N][K16]
+ *   packed f16:  weights [B][2][M][K16], data [B][2][K][Np] (N-contiguous, Np >= N)
  *   packed b1:   weights [B][2][M][Kw],  data transposed [B][2][N][Kw]
  *                LSB-first uint32 words along K, padding bits 0.
  *   outputs:     [B][2][n_rows][N]   (row subset `rows` of the M beams)
@@ -280,19 +280,17 @@ int oracle_cgemm_b1_packed(const uint32_t* wp, const uint32_t* xp, int64_t M, in
 /* operand 1 = data [B][K][N] -> transposed [B][2][N][Kp].                    */
 /* ------------------------------------------------------------------------ */
 int oracle_pack_f16(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
-                    int64_t K16, uint16_t* dst) {
-  if (!src || !dst || B < 1 || R < 1 || C < 1) return OR_EINVAL;
-  int64_t rows = operand == 0 ? R : C;      /* M for weights, N for data */
-  int64_t K = operand == 0 ? C : R;
-  if (K16 < K) return OR_EINVAL;
-  memset(dst, 0, sizeof(uint16_t) * (size_t)(B * 2 * rows * K16));
+                    int64_t Cp, uint16_t* dst) {
+  /* Both operands keep their row order: weights [B][M][K] -> [B][2][M][Cp = K16],
+     data [B][K][N] -> [B][2][K][Cp = Np]; columns C..Cp-1 are 0.0 (operand only names them). */
+  (void)operand;
+  if (!src || !dst || B < 1 || R < 1 || C < 1 || Cp < C) return OR_EINVAL;
+  memset(dst, 0, sizeof(uint16_t) * (size_t)(B * 2 * R * Cp));
   for (int64_t b = 0; b < B; ++b)
     for (int64_t r = 0; r < R; ++r)
       for (int64_t c = 0; c < C; ++c) {
-        int64_t row = operand == 0 ? r : c;
-        int64_t k = operand == 0 ? c : r;
-        dst[((b * 2 + 0) * rows + row) * K16 + k] = oracle_f32_to_f16(src_re(src, layout, b, r, c, R, C));
-        dst[((b * 2 + 1) * rows + row) * K16 + k] = oracle_f32_to_f16(src_im(src, layout, b, r, c, R, C));
+        dst[((b * 2 + 0) * R + r) * Cp + c] = oracle_f32_to_f16(src_re(src, layout, b, r, c, R, C));
+        dst[((b * 2 + 1) * R + r) * Cp + c] = oracle_f32_to_f16(src_im(src, layout, b, r, c, R, C));
       }
   return OR_OK;
 }

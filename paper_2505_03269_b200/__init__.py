@@ -112,6 +112,7 @@ class Plan:
         self.w_bytes, self.x_bytes, self.out_bytes, self.k_packed = layout_sizes(
             self.M, self.N, self.K, self.batch, self.precision)
         self.variant = lib().tcbf_plan_variant(h).decode()
+        self.n_packed = (self.N + 7) // 8 * 8   # F16 data rows (MN-major packed data)
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
@@ -122,8 +123,11 @@ class Plan:
 
     # ------------------------------------------------------------ buffers (torch = plumbing)
     def packed_shape(self, operand):
-        rows = self.M if operand == WEIGHTS else self.N
-        return (self.batch, 2, rows, self.k_packed)
+        if operand == WEIGHTS:
+            return (self.batch, 2, self.M, self.k_packed)
+        if self.precision == F16:
+            return (self.batch, 2, self.K, self.n_packed)   # MN-major: [K][Np]
+        return (self.batch, 2, self.N, self.k_packed)       # bits along K: [N][Kw]
 
     def alloc_packed(self, operand, device="cuda"):
         import torch

@@ -9,13 +9,16 @@
 //
 // B200 design (not the paper's WMMA design, PAPER.md:416 lists this as future work):
 //   * persistent CTAs (grid = #SMs), static batch-major tile schedule (PAPER.md:101 batch);
-//   * warp 0: TMA producer filling a STAGES-deep smem ring (A_r, A_i, B_r, B_i tiles,
-//     128-byte swizzle), mbarrier full/empty pipeline (replaces the paper's cp.async
-//     multi-buffer);
+//   * warp 0: TMA producer filling a STAGES-deep smem ring (A_r, A_i K-major boxes and B_r, B_i
+//     MN-major boxes, 128-byte swizzle), mbarrier full/empty pipeline (replaces the paper's
+//     cp.async multi-buffer);
 //   * warp 1: one thread issues tcgen05.mma (M=128, N=BN, K=16) into TMEM; TMEM holds two
 //     accumulator sets (D_r, D_i) so the epilogue of tile i overlaps the mainloop of i+1;
-//   * warps 2-5: epilogue, tcgen05.ld -> registers -> swizzled smem -> TMA bulk store of
-//     the fp32 planar output (the dominant HBM traffic for the radio shapes).
+//   * warps 2..2+EPI_WARPS-1: epilogue, tcgen05.ld -> registers -> swizzled smem -> TMA bulk
+//     store of the fp32 planar output (the dominant HBM traffic for the radio shapes).  With 8
+//     epilogue warps two warps share each TMEM lane quadrant and split the columns.
+// The data operand is consumed MN-major ([K][N], N contiguous), so tcbf_pack(DATA) is a pure
+// streaming conversion without the transpose of the paper's design.
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -27,27 +30,58 @@ namespace tcbf {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 64;  // fp16 elements per 128-byte swizzle row
-constexpr int NUM_THREADS = 192;
 
-template <int BN, int STAGES, bool TMA_STORE>
+template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
 struct F16Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-  static constexpr int EPI_BYTES = TMA_STORE ? 4 * 2 * 4096 : 0;
+  static constexpr int EPI_BUFS = 2;
+  static constexpr int EPI_BYTES = TMA_STORE ? EPI_WARPS * EPI_BUFS * 4096 : 0;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x (D_r, D_i)
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+  static constexpr int NUM_THREADS = (2 + EPI_WARPS) * 32;
   static_assert(TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation must be a power of two");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+  static_assert(BK == 32 || BK == 64, "BK");
+  static_assert(BN % 64 == 0, "MN-major B operand is loaded in 64-column blocks");
 };
 
-template <int BN, int STAGES, bool TMA_STORE>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+// K-major A operand, swizzle width = BK*2 bytes (64 B -> SWIZZLE_64B, 128 B -> SWIZZLE_128B).
+template <int BK>
+__device__ __forceinline__ uint64_t desc_a(const void* tile, uint32_t k_byte_off) {
+  uint32_t addr = smem_u32(tile) + k_byte_off;
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;                               // LBO (unused, swizzled K-major)
+  d |= (uint64_t)((8u * BK * 2) >> 4) << 32;             // SBO: 8 rows of BK*2 bytes
+  d |= (uint64_t)1u << 46;                               // version
+  d |= (uint64_t)(BK == 64 ? 2u : 4u) << 61;             // SWIZZLE_128B / SWIZZLE_64B
+  return d;
+}
+// MN-major B operand: 64-element (128 B) MN blocks of BK k-rows each, 128-byte swizzle.
+// LBO = distance between MN blocks (BK rows x 128 B), SBO = 8 k-rows (1024 B).
+template <int BK>
+__device__ __forceinline__ uint64_t desc_b_mn(const void* tile, uint32_t k_row) {
+  uint32_t addr = smem_u32(tile) + k_row * 128u;
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((BK * 128u) >> 4) << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_f16_mn(uint32_t M, uint32_t N, bool negate_a) {
+  return (1u << 4) | ((negate_a ? 1u : 0u) << 13) | (0u << 15) /* A K-major */ | (1u << 16) /* B MN-major */ |
+         ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
+__global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::NUM_THREADS, 1)
     cgemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, GemmF16Args args) {
-  using Cfg = F16Cfg<BN, STAGES, TMA_STORE>;
+  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_base = smem + STAGES * Cfg::STAGE_BYTES;
@@ -67,7 +101,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);
+      mbar_init(&tempty_bar[s], EPI_WARPS);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -101,8 +135,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           tma_load_3d(st, &tmA, &full_bar[stage], kb * BK, m0, 2 * b);
           tma_load_3d(st + Cfg::A_BYTES, &tmA, &full_bar[stage], kb * BK, m0, 2 * b + 1);
-          tma_load_3d(st + 2 * Cfg::A_BYTES, &tmB, &full_bar[stage], kb * BK, n0, 2 * b);
-          tma_load_3d(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &tmB, &full_bar[stage], kb * BK, n0, 2 * b + 1);
+          uint8_t* sb = st + 2 * Cfg::A_BYTES;
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) {
+            tma_load_3d(sb + j * BK * 128, &tmB, &full_bar[stage], n0 + 64 * j, kb * BK, 2 * b);
+            tma_load_3d(sb + Cfg::B_BYTES + j * BK * 128, &tmB, &full_bar[stage], n0 + 64 * j, kb * BK, 2 * b + 1);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -110,8 +148,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_f16(BM, BN, false);
-      constexpr uint32_t IDESC_NEG = idesc_f16(BM, BN, true);
+      constexpr uint32_t IDESC = idesc_f16_mn(BM, BN, false);
+      constexpr uint32_t IDESC_NEG = idesc_f16_mn(BM, BN, true);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -132,9 +170,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint8_t* sBi = sBr + Cfg::B_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint32_t off = kk * 32;
-            const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
-            const uint64_t br = smem_desc_k128(sBr, off), bi = smem_desc_k128(sBi, off);
+            const uint64_t ar = desc_a<BK>(sAr, kk * 32), ai = desc_a<BK>(sAi, kk * 32);
+            const uint64_t br = desc_b_mn<BK>(sBr, kk * 16), bi = desc_b_mn<BK>(sBi, kk * 16);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             mma_f16_ss(d_re, ar, br, IDESC, acc);     // Re += Re(a) Re(b)
             mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);  // Re += -Im(a) Im(b)
@@ -148,10 +185,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;        // TMEM lane quadrant this warp may access
-    const int ew = warp - 2;       // private staging buffers
-    uint8_t* stg = epi_base + ew * 8192;
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;               // TMEM lane quadrant this warp may access
+    const int ew = warp - 2;              // private staging buffers
+    const int half = ew / 4;              // which columns of the quadrant (8 warps: 2 halves)
+    constexpr int SPLIT = EPI_WARPS / 4;  // 1 or 2 warps per quadrant
+    constexpr int CHUNKS = BN / 32;
+    constexpr int MY_CHUNKS = 2 * CHUNKS / SPLIT;
+    uint8_t* stg = epi_base + ew * (Cfg::EPI_BUFS * 4096);
     int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
@@ -162,28 +203,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int abuf = it & 1;
       mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
       tc_fence_after();
-      constexpr int CHUNKS = BN / 32;
-#pragma unroll 1
-      for (int ch = 0; ch < 2 * CHUNKS; ++ch) {
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN;
+      uint32_t v[2][32];
+      // chunk i of this warp: global chunk ch = i * SPLIT + half (interleaved column split)
+      tmem_ld_32x32b_x32(tbase + (0 * SPLIT + half) * 32, v[0]);
+#pragma unroll
+      for (int i = 0; i < MY_CHUNKS; ++i) {
+        const int ch = i * SPLIT + half;
         const int part = ch / CHUNKS;  // 0 = Re, 1 = Im
         const int c = ch % CHUNKS;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN + part * BN + c * 32, v);
         tmem_wait_ld();
-        if (ch == 2 * CHUNKS - 1) {  // all TMEM reads of this tile done: release the buffer
+        if (i + 1 < MY_CHUNKS) {
+          tmem_ld_32x32b_x32(tbase + ((i + 1) * SPLIT + half) * 32, v[(i + 1) & 1]);
+        } else {  // all TMEM reads of this tile issued and complete: release the buffer
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
+        const uint32_t* vv = v[i & 1];
         if constexpr (TMA_STORE) {
-          if (lane == 0) bulk_wait_group_read<1>();
+          if (lane == 0) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();
           __syncwarp();
           uint8_t* buf = stg + sbuf * 4096;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int pos = j ^ (lane & 7);  // 128-byte swizzle, matches the tensor map
             *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
-                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -191,7 +237,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
             bulk_commit_group();
           }
-          sbuf ^= 1;
+          sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
         } else {
           const int m = m0 + q * 32 + lane;
           if (m < args.M) {
@@ -199,7 +245,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = n0 + c * 32 + j;
-              if (n < args.N) row[n] = __uint_as_float(v[j]);
+              if (n < args.N) row[n] = __uint_as_float(vv[j]);
             }
           }
         }
@@ -219,31 +265,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int BN, int STAGES, bool TMA_STORE>
+template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                         const GemmF16Args& args, int num_sms, cudaStream_t stream) {
-  using Cfg = F16Cfg<BN, STAGES, TMA_STORE>;
-  auto kern = cgemm_f16_kernel<BN, STAGES, TMA_STORE>;
+  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
+  auto kern = cgemm_f16_kernel<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   int grid = args.num_tiles < num_sms ? args.num_tiles : num_sms;
-  kern<<<grid, NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, args);
+  kern<<<grid, Cfg::NUM_THREADS, Cfg::SMEM_BYTES, stream>>>(tmA, tmB, tmC, args);
   return cudaGetLastError();
+}
+
+template <bool TS>
+cudaError_t dispatch(int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                     const GemmF16Args& g, int sms, cudaStream_t s) {
+  switch (variant) {
+    case F16_V_N64:      return launch_impl<64, 64, 4, 4, TS>(a, b, c, g, sms, s);
+    case F16_V_K64_S3:   return launch_impl<128, 64, 3, 4, TS>(a, b, c, g, sms, s);
+    case F16_V_K32_S4_E8: return launch_impl<128, 32, 4, 8, TS>(a, b, c, g, sms, s);
+    case F16_V_K64_S2_E8: return launch_impl<128, 64, 2, 8, TS>(a, b, c, g, sms, s);
+    case F16_V_K32_S6_E4: return launch_impl<128, 32, 6, 4, TS>(a, b, c, g, sms, s);
+    default:             return launch_impl<128, 32, 4, 8, TS>(a, b, c, g, sms, s);
+  }
 }
 
 }  // namespace
 
-int gemm_f16_block_n(int variant) { return variant == 64 ? 64 : 128; }
+int gemm_f16_block_n(int variant) { return variant == F16_V_N64 ? 64 : 128; }
 
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                            const GemmF16Args& args, int block_n, bool tma_store, int num_sms,
+                            const GemmF16Args& args, int variant, bool tma_store, int num_sms,
                             cudaStream_t stream) {
-  if (block_n == 64) {
-    return tma_store ? launch_impl<64, 4, true>(tmA, tmB, tmC, args, num_sms, stream)
-                     : launch_impl<64, 4, false>(tmA, tmB, tmC, args, num_sms, stream);
-  }
-  return tma_store ? launch_impl<128, 3, true>(tmA, tmB, tmC, args, num_sms, stream)
-                   : launch_impl<128, 3, false>(tmA, tmB, tmC, args, num_sms, stream);
+  return tma_store ? dispatch<true>(variant, tmA, tmB, tmC, args, num_sms, stream)
+                   : dispatch<false>(variant, tmA, tmB, tmC, args, num_sms, stream);
+}
+
+int gemm_f16_block_k(int variant) {
+  return (variant == F16_V_K32_S4_E8 || variant == F16_V_K32_S6_E4) ? 32 : 64;
 }
 
 }  // namespace tcbf

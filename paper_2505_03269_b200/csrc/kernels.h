@@ -13,8 +13,19 @@ struct GemmF16Args {
   float* out;  // used by the masked-store epilogue (N % 4 != 0)
 };
 
+// fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
+enum {
+  F16_V_K32_S4_E8 = 0,  // 128x128, BK 32, 4 stages, 8 epilogue warps (default)
+  F16_V_K64_S3 = 1,     // 128x128, BK 64, 3 stages, 4 epilogue warps
+  F16_V_K64_S2_E8 = 2,  // 128x128, BK 64, 2 stages, 8 epilogue warps
+  F16_V_K32_S6_E4 = 3,  // 128x128, BK 32, 6 stages, 4 epilogue warps
+  F16_V_N64 = 4,        // 128x64,  BK 64, 4 stages, 4 epilogue warps (small N)
+  F16_V_COUNT = 5
+};
+int gemm_f16_block_n(int variant);
+int gemm_f16_block_k(int variant);
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                            const GemmF16Args& args, int block_n, bool tma_store, int num_sms,
+                            const GemmF16Args& args, int variant, bool tma_store, int num_sms,
                             cudaStream_t stream);
 
 struct GemmB1Args {

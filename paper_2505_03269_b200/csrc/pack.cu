@@ -10,6 +10,7 @@
 //        bits 0, Kp = round_up(ceil(K/32), 8) words (256-bit granule).
 // Weights [B][M][K] keep their row order; data [B][K][N] is transposed to [B][2][N][Kp]
 // so both GEMM operands are K-major (what the tcgen05 smem descriptors and TMA want).
+#include <algorithm>
 #include <cstdint>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -31,72 +32,49 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// weights: [B][M][K] -> [B][2][M][K16]; one thread per 8 consecutive k.
-template <int LAYOUT>
-__global__ void pack_f16_rows(const float* __restrict__ src, int64_t B, int64_t M, int64_t K, int64_t K16,
-                              uint16_t* __restrict__ dst) {
-  const int64_t groups = K16 / 8;
-  const int64_t total = B * M * groups;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t g = i % groups;
-    const int64_t bm = i / groups;
-    const int64_t m = bm % M;
-    const int64_t b = bm / M;
-    float re[8], im[8];
+// [B][R][C] fp32 complex -> [B][2][R][Cp] fp16 planar, zero tail C..Cp-1; one thread per 8
+// consecutive elements of a row, rows distributed over blocks (no 64-bit divisions per element).
+// Used for the weights (R = M, C = K, Cp = K16: K-major A operand) and for the data (R = K,
+// C = N, Cp = Np: the GEMM reads the data MN-major, so no transpose is needed).
+template <int LAYOUT, bool VEC>
+__global__ void __launch_bounds__(256) pack_f16_rows(const float* __restrict__ src, int64_t rows, int64_t R,
+                                                     int64_t C, int64_t Cp, uint16_t* __restrict__ dst) {
+  const int groups = (int)(Cp / 8);
+  const int rpb = groups >= 256 ? 1 : 256 / groups;  // rows per block pass
+  const int lr = threadIdx.x / groups;
+  const int g0 = threadIdx.x - lr * groups;
+  for (int64_t row0 = (int64_t)blockIdx.x * rpb; row0 < rows; row0 += (int64_t)gridDim.x * rpb) {
+    const int64_t row = row0 + lr;
+    if (lr >= rpb || row >= rows) continue;
+    const int64_t b = row / R, r = row - b * R;
+    for (int g = g0; g < groups; g += (groups >= 256 ? 256 : groups)) {
+      const int64_t c0 = (int64_t)g * 8;
+      float re[8], im[8];
+      if (VEC && LAYOUT == 0 && c0 + 8 <= C) {
+        const float4* p = reinterpret_cast<const float4*>(src + ((b * R + r) * C + c0) * 2);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t k = g * 8 + j;
-      if (k < K) {
-        float2 v = load_c<LAYOUT>(src, b, m, k, M, K);
-        re[j] = v.x;
-        im[j] = v.y;
+        for (int j = 0; j < 4; ++j) {
+          float4 v = __ldg(p + j);
+          re[2 * j] = v.x; im[2 * j] = v.y; re[2 * j + 1] = v.z; im[2 * j + 1] = v.w;
+        }
       } else {
-        re[j] = 0.f;
-        im[j] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (c0 + j < C) {
+            float2 v = load_c<LAYOUT>(src, b, r, c0 + j, R, C);
+            re[j] = v.x;
+            im[j] = v.y;
+          } else {
+            re[j] = 0.f;
+            im[j] = 0.f;
+          }
+        }
       }
+      uint4 pr = make_uint4(h2u(re[0], re[1]), h2u(re[2], re[3]), h2u(re[4], re[5]), h2u(re[6], re[7]));
+      uint4 pi = make_uint4(h2u(im[0], im[1]), h2u(im[2], im[3]), h2u(im[4], im[5]), h2u(im[6], im[7]));
+      *reinterpret_cast<uint4*>(dst + ((b * 2 + 0) * R + r) * Cp + c0) = pr;
+      *reinterpret_cast<uint4*>(dst + ((b * 2 + 1) * R + r) * Cp + c0) = pi;
     }
-    uint4 pr = make_uint4(h2u(re[0], re[1]), h2u(re[2], re[3]), h2u(re[4], re[5]), h2u(re[6], re[7]));
-    uint4 pi = make_uint4(h2u(im[0], im[1]), h2u(im[2], im[3]), h2u(im[4], im[5]), h2u(im[6], im[7]));
-    *reinterpret_cast<uint4*>(dst + ((b * 2 + 0) * M + m) * K16 + g * 8) = pr;
-    *reinterpret_cast<uint4*>(dst + ((b * 2 + 1) * M + m) * K16 + g * 8) = pi;
-  }
-}
-
-// data: [B][K][N] -> [B][2][N][K16]; 64(k) x 32(n) tile through shared memory.
-template <int LAYOUT>
-__global__ void __launch_bounds__(256) pack_f16_transpose(const float* __restrict__ src, int64_t B, int64_t K,
-                                                          int64_t N, int64_t K16, uint16_t* __restrict__ dst) {
-  __shared__ __half sre[64][40];
-  __shared__ __half sim[64][40];
-  const int64_t n0 = (int64_t)blockIdx.x * 32;
-  for (int64_t b = blockIdx.z; b < B; b += gridDim.z)
-  for (int64_t k0 = (int64_t)blockIdx.y * 64; k0 < K16; k0 += (int64_t)gridDim.y * 64) {
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    const int kl = ty + 8 * r;
-    const int64_t k = k0 + kl, n = n0 + tx;
-    float2 v = make_float2(0.f, 0.f);
-    if (k < K && n < N) v = load_c<LAYOUT>(src, b, k, n, K, N);
-    sre[kl][tx] = __float2half_rn(v.x);
-    sim[kl][tx] = __float2half_rn(v.y);
-  }
-  __syncthreads();
-  const int nl = threadIdx.x >> 3, kg = threadIdx.x & 7;
-  const int64_t n = n0 + nl;
-  if (n < N) {
-    uint32_t wr[4], wi[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      __half2 hr = __halves2half2(sre[kg * 8 + 2 * j][nl], sre[kg * 8 + 2 * j + 1][nl]);
-      __half2 hi = __halves2half2(sim[kg * 8 + 2 * j][nl], sim[kg * 8 + 2 * j + 1][nl]);
-      wr[j] = *reinterpret_cast<uint32_t*>(&hr);
-      wi[j] = *reinterpret_cast<uint32_t*>(&hi);
-    }
-    *reinterpret_cast<uint4*>(dst + ((b * 2 + 0) * N + n) * K16 + k0 + kg * 8) = make_uint4(wr[0], wr[1], wr[2], wr[3]);
-    *reinterpret_cast<uint4*>(dst + ((b * 2 + 1) * N + n) * K16 + k0 + kg * 8) = make_uint4(wi[0], wi[1], wi[2], wi[3]);
-  }
-  __syncthreads();
   }
 }
 
@@ -163,15 +141,18 @@ inline int64_t cap_dim(int64_t v) { return v < 65535 ? (v < 1 ? 1 : v) : 65535; 
 }  // namespace
 
 cudaError_t launch_pack_f16(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
-                            int64_t K16, uint16_t* dst, cudaStream_t stream) {
-  if (operand == 0) {  // weights, R = M, C = K
-    const int64_t work = B * R * (K16 / 8);
-    if (layout == 0) pack_f16_rows<0><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, K16, dst);
-    else pack_f16_rows<1><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, K16, dst);
-  } else {  // data, R = K, C = N
-    dim3 grid((unsigned)((C + 31) / 32), (unsigned)cap_dim(K16 / 64), (unsigned)cap_dim(B));
-    if (layout == 0) pack_f16_transpose<0><<<grid, 256, 0, stream>>>(src, B, R, C, K16, dst);
-    else pack_f16_transpose<1><<<grid, 256, 0, stream>>>(src, B, R, C, K16, dst);
+                            int64_t Cp, uint16_t* dst, cudaStream_t stream) {
+  (void)operand;  // weights: R=M, C=K, Cp=K16; data: R=K, C=N, Cp=Np -- the same row conversion
+  const int64_t rows = B * R;
+  const int64_t groups = Cp / 8;
+  const int64_t rpb = groups >= 256 ? 1 : 256 / groups;
+  const int64_t blocks = std::min<int64_t>((rows + rpb - 1) / rpb, 148LL * 16);
+  const bool vec = (C % 2 == 0) && (reinterpret_cast<uintptr_t>(src) % 16 == 0);
+  if (layout == 0) {
+    if (vec) pack_f16_rows<0, true><<<(unsigned)blocks, 256, 0, stream>>>(src, rows, R, C, Cp, dst);
+    else pack_f16_rows<0, false><<<(unsigned)blocks, 256, 0, stream>>>(src, rows, R, C, Cp, dst);
+  } else {
+    pack_f16_rows<1, false><<<(unsigned)blocks, 256, 0, stream>>>(src, rows, R, C, Cp, dst);
   }
   return cudaGetLastError();
 }

@@ -54,8 +54,12 @@ tcbf_status compute_sizes(int64_t M, int64_t N, int64_t K, int64_t B, tcbf_preci
   size_t t, w, x, o;
   if (!mul_ok((size_t)B * 2, (size_t)M, &t) || !mul_ok(t, (size_t)k, &t) || !mul_ok(t, elem, &w))
     return fail(TCBF_ERR_INVALID_ARG, "packed weight size overflows size_t");
-  if (!mul_ok((size_t)B * 2, (size_t)N, &t) || !mul_ok(t, (size_t)k, &t) || !mul_ok(t, elem, &x))
-    return fail(TCBF_ERR_INVALID_ARG, "packed data size overflows size_t");
+  // F16 data is consumed MN-major: [B][2][K][Np], Np = round_up(N, 8); B1 data is [B][2][N][Kw]
+  const bool dx_ok = p == TCBF_PREC_F16
+                         ? (mul_ok((size_t)B * 2, (size_t)K, &t) && mul_ok(t, (size_t)((N + 7) / 8 * 8), &t) &&
+                            mul_ok(t, elem, &x))
+                         : (mul_ok((size_t)B * 2, (size_t)N, &t) && mul_ok(t, (size_t)k, &t) && mul_ok(t, elem, &x));
+  if (!dx_ok) return fail(TCBF_ERR_INVALID_ARG, "packed data size overflows size_t");
   if (!mul_ok((size_t)B * 2, (size_t)M, &t) || !mul_ok(t, (size_t)N, &t) || !mul_ok(t, 4, &o))
     return fail(TCBF_ERR_INVALID_ARG, "output size overflows size_t");
   if (wb) *wb = w;
@@ -147,11 +151,12 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   p->device = dev;
   p->num_sms = sms;
   p->w_bytes = wb; p->x_bytes = xb; p->out_bytes = ob;
-  // fp16 tile width: BN = 128 unless N is small enough that 64 wastes less (e.g. N <= 64)
-  p->block_n = N <= 64 ? 64 : 128;
-  if (const char* env = getenv("TCBF_F16_BLOCK_N")) {
+  p->n_packed = (N + 7) / 8 * 8;
+  // fp16 kernel variant: 128x64 tiles when N <= 64, else 128x128 (BK 32, 4 stages, 8 epilogue warps)
+  p->f16_variant = N <= 64 ? tcbf::F16_V_N64 : tcbf::F16_V_K32_S4_E8;
+  if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
-    if (v == 64 || v == 128) p->block_n = v;
+    if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
   }
   p->b1_tc = 1;
   if (const char* env = getenv("TCBF_B1_KERNEL")) p->b1_tc = strcmp(env, "popc") == 0 ? 0 : 1;
@@ -183,8 +188,12 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
-  if (plan->N % 4 != 0) return plan->block_n == 64 ? "f16_tcgen05_128x64_stg" : "f16_tcgen05_128x128_stg";
-  return plan->block_n == 64 ? "f16_tcgen05_128x64_tma" : "f16_tcgen05_128x128_tma";
+  static const char* names[2][tcbf::F16_V_COUNT] = {
+      {"f16_tcgen05_128x128_k32s4e8_stg", "f16_tcgen05_128x128_k64s3e4_stg", "f16_tcgen05_128x128_k64s2e8_stg",
+       "f16_tcgen05_128x128_k32s6e4_stg", "f16_tcgen05_128x64_k64s4e4_stg"},
+      {"f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
+       "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma"}};
+  return names[plan->N % 4 == 0 ? 1 : 0][plan->f16_variant];
 }
 
 tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src, tcbf_src_layout layout,
@@ -203,7 +212,8 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (plan->prec == TCBF_PREC_F16)
-    e = tcbf::launch_pack_f16(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, static_cast<uint16_t*>(dst), st);
+    e = tcbf::launch_pack_f16(src, (int)layout, (int)operand, plan->B, R, C,
+                              operand == TCBF_WEIGHTS ? plan->kp : plan->n_packed, static_cast<uint16_t*>(dst), st);
   else
     e = tcbf::launch_pack_b1(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, static_cast<uint32_t*>(dst), st);
   if (e != cudaSuccess) return cuda_fail(e, "pack kernel launch");
@@ -221,13 +231,18 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (plan->prec == TCBF_PREC_F16) {
-    const int bn = plan->block_n;
+    const int var = plan->f16_variant;
+    const int bn = tcbf::gemm_f16_block_n(var);
+    const int bk = tcbf::gemm_f16_block_k(var);
     const bool tma_store = (plan->N % 4) == 0;
     CUtensorMap ta, tb, tc;
-    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    // A (weights, K-major [2B][M][K16]): box {BK, 128}, swizzle = BK * 2 bytes
+    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
+                  bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
-    s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->kp, plan->N, 2 * plan->B, 64, bn,
+    // B (data, MN-major [2B][K][Np]): box {64 columns, BK rows}, 128-byte swizzle; K tail is OOB -> 0
+    s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->n_packed, plan->K, 2 * plan->B, 64, bk,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
     if (tma_store) {
@@ -244,9 +259,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
     if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
     a.num_tiles = (int)nt;
-    a.num_kb = (int)(plan->kp / 64);
+    a.num_kb = (int)(plan->kp / bk);
     a.out = static_cast<float*>(out);
-    e = tcbf::launch_gemm_f16(ta, tb, tc, a, bn, tma_store, plan->num_sms, st);
+    e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, tma_store, plan->num_sms, st);
   } else {
     tcbf::GemmB1Args a;
     a.w = static_cast<const uint32_t*>(w_packed);

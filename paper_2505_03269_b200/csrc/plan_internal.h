@@ -11,7 +11,8 @@ struct tcbf_plan_s {
   int64_t kp;   // K16 (fp16 elements) or Kw (uint32 words)
   int device;
   int num_sms;
-  int block_n;  // fp16 GEMM tile width
+  int f16_variant;  // tcbf::F16_V_*
+  int64_t n_packed;  // F16 data row length Np = round_up(N, 8) (MN-major packed data)
   int b1_tc;    // 1 = tensor-core (kind::i8) 1-bit kernel, 0 = CUDA-core popc kernel
   size_t w_bytes, x_bytes, out_bytes;
 };

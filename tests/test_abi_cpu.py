@@ -35,8 +35,8 @@ def test_layout_sizes(tcbf):
     # F16: Kp = round_up(K, 64); bytes = B*2*rows*Kp*2; out = B*2*M*N*4
     w, x, o, k = tcbf.layout_sizes(1024, 1024, 256, 256, "f16")
     assert k == 256 and w == 256 * 2 * 1024 * 256 * 2 and x == w and o == 256 * 2 * 1024 * 1024 * 4
-    w, x, o, k = tcbf.layout_sizes(3, 5, 65, 2, "f16")
-    assert k == 128 and w == 2 * 2 * 3 * 128 * 2 and x == 2 * 2 * 5 * 128 * 2 and o == 2 * 2 * 3 * 5 * 4
+    w, x, o, k = tcbf.layout_sizes(3, 5, 65, 2, "f16")   # data is [B][2][K][round_up(N, 8)]
+    assert k == 128 and w == 2 * 2 * 3 * 128 * 2 and x == 2 * 2 * 65 * 8 * 2 and o == 2 * 2 * 3 * 5 * 4
     # B1: Kw = round_up(ceil(K/32), 8) words
     w, x, o, k = tcbf.layout_sizes(1024, 4096, 512, 256, "b1")
     assert k == 16 and w == 256 * 2 * 1024 * 16 * 4 and x == 256 * 2 * 4096 * 16 * 4

@@ -77,7 +77,7 @@ def test_pack_f16_bit_exact(tcbf, layout, shape):
     wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout).cpu().numpy().view(np.uint16)
     xp = plan.pack(tcbf.DATA, _dev(conv(x)), layout).cpu().numpy().view(np.uint16)
     assert np.array_equal(wp, oracle.pack_f16(conv(w), lay, oracle.WEIGHTS, B, M, K, plan.k_packed))
-    assert np.array_equal(xp, oracle.pack_f16(conv(x), lay, oracle.DATA, B, K, N, plan.k_packed))
+    assert np.array_equal(xp, oracle.pack_f16(conv(x), lay, oracle.DATA, B, K, N, plan.n_packed))
 
 
 def test_pack_f16_special_values(tcbf):

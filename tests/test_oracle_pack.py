@@ -9,18 +9,18 @@ import synth
 
 def test_pack_f16_weights_and_data_vs_numpy():
     B, M, K, N = 2, 5, 70, 9
-    K16 = 128
+    K16, Np = 128, 16
     w = synth.generate("uniform", 3, 0, B, M, K)
     x = synth.generate("uniform", 3, 1, B, K, N)
     for layout, conv in ((0, synth.to_interleaved), (1, synth.to_planar)):
         pw = oracle.pack_f16(conv(w), layout, oracle.WEIGHTS, B, M, K, K16)
-        px = oracle.pack_f16(conv(x), layout, oracle.DATA, B, K, N, K16)
+        px = oracle.pack_f16(conv(x), layout, oracle.DATA, B, K, N, Np)
         ew = np.zeros((B, 2, M, K16), np.float16)
         ew[:, 0, :, :K] = w.real.astype(np.float16)
         ew[:, 1, :, :K] = w.imag.astype(np.float16)
-        ex = np.zeros((B, 2, N, K16), np.float16)
-        ex[:, 0, :, :K] = x.real.transpose(0, 2, 1).astype(np.float16)
-        ex[:, 1, :, :K] = x.imag.transpose(0, 2, 1).astype(np.float16)
+        ex = np.zeros((B, 2, K, Np), np.float16)
+        ex[:, 0, :, :N] = x.real.astype(np.float16)
+        ex[:, 1, :, :N] = x.imag.astype(np.float16)
         assert np.array_equal(pw, ew.view(np.uint16))
         assert np.array_equal(px, ex.view(np.uint16))
 
