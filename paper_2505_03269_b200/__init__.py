@@ -115,8 +115,11 @@ class Plan:
         self.n_packed = (self.N + 7) // 8 * 8   # F16 data rows (MN-major packed data)
 
     def close(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
-            lib().tcbf_plan_destroy(self._h)
+        if getattr(self, "_h", None) is not None and self._h.value and _LIB is not None:
+            try:
+                _LIB.tcbf_plan_destroy(self._h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     __del__ = close

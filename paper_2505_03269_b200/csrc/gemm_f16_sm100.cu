@@ -31,13 +31,15 @@ namespace {
 
 constexpr int BM = 128;
 
-template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
+template <int BN, int BK, int STAGES, int EPI_WARPS, int EPI>
 struct F16Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int EPI_BUFS = 2;
-  static constexpr int EPI_BYTES = TMA_STORE ? EPI_WARPS * EPI_BUFS * 4096 : 0;
+  // EPI: 0 = swizzled smem staging + TMA bulk store, 1 = direct 256-bit st.global from
+  // registers (no smem traffic; needs N % 8 == 0), 2 = masked scalar stores (any N)
+  static constexpr int EPI_BYTES = EPI == 0 ? EPI_WARPS * EPI_BUFS * 4096 : 0;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x (D_r, D_i)
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
@@ -77,11 +79,11 @@ __host__ __device__ constexpr uint32_t idesc_f16_mn(uint32_t M, uint32_t N, bool
          ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
-template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
-__global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::NUM_THREADS, 1)
+template <int BN, int BK, int STAGES, int EPI_WARPS, int EPI>
+__global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_THREADS, 1)
     cgemm_f16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, GemmF16Args args) {
-  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
+  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* epi_base = smem + STAGES * Cfg::STAGE_BYTES;
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (TMA_STORE) tma_prefetch_desc(&tmC);
+    if (EPI == 0) tma_prefetch_desc(&tmC);
   }
   if (warp == 1) {
     tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
@@ -173,6 +175,7 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
             const uint64_t ar = desc_a<BK>(sAr, kk * 32), ai = desc_a<BK>(sAi, kk * 32);
             const uint64_t br = desc_b_mn<BK>(sBr, kk * 16), bi = desc_b_mn<BK>(sBi, kk * 16);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
+            if (args.debug & 2) continue;
             mma_f16_ss(d_re, ar, br, IDESC, acc);     // Re += Re(a) Re(b)
             mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);  // Re += -Im(a) Im(b)
             mma_f16_ss(d_im, ar, bi, IDESC, acc);     // Im += Re(a) Im(b)
@@ -221,7 +224,8 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
         const uint32_t* vv = v[i & 1];
-        if constexpr (TMA_STORE) {
+        if (args.debug & 1) continue;
+        if constexpr (EPI == 0) {
           if (lane == 0) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();
           __syncwarp();
           uint8_t* buf = stg + sbuf * 4096;
@@ -238,6 +242,20 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
             bulk_commit_group();
           }
           sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
+        } else if constexpr (EPI == 1) {
+          const int m = m0 + q * 32 + lane;
+          const int nb = n0 + c * 32;
+          if (m < args.M) {
+            float* row = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
+            if (nb + 32 <= args.N) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (nb + j < args.N) row[j] = __uint_as_float(vv[j]);
+            }
+          }
         } else {
           const int m = m0 + q * 32 + lane;
           if (m < args.M) {
@@ -251,7 +269,7 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
         }
       }
     }
-    if constexpr (TMA_STORE) {
+    if constexpr (EPI == 0) {
       if (lane == 0) bulk_wait_group<0>();
       __syncwarp();
     }
@@ -265,11 +283,11 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>::
   }
 }
 
-template <int BN, int BK, int STAGES, int EPI_WARPS, bool TMA_STORE>
+template <int BN, int BK, int STAGES, int EPI_WARPS, int EPI>
 cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                         const GemmF16Args& args, int num_sms, cudaStream_t stream) {
-  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
-  auto kern = cgemm_f16_kernel<BN, BK, STAGES, EPI_WARPS, TMA_STORE>;
+  using Cfg = F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>;
+  auto kern = cgemm_f16_kernel<BN, BK, STAGES, EPI_WARPS, EPI>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   int grid = args.num_tiles < num_sms ? args.num_tiles : num_sms;
@@ -277,16 +295,21 @@ cudaError_t launch_impl(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
   return cudaGetLastError();
 }
 
-template <bool TS>
-cudaError_t dispatch(int variant, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+cudaError_t dispatch(int variant, int epi, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                      const GemmF16Args& g, int sms, cudaStream_t s) {
+  if (epi == 2) {  // N % 8 != 0: masked stores
+    return variant == F16_V_N64 ? launch_impl<64, 64, 4, 4, 2>(a, b, c, g, sms, s)
+                                : launch_impl<128, 64, 3, 4, 2>(a, b, c, g, sms, s);
+  }
   switch (variant) {
-    case F16_V_N64:      return launch_impl<64, 64, 4, 4, TS>(a, b, c, g, sms, s);
-    case F16_V_K64_S3:   return launch_impl<128, 64, 3, 4, TS>(a, b, c, g, sms, s);
-    case F16_V_K32_S4_E8: return launch_impl<128, 32, 4, 8, TS>(a, b, c, g, sms, s);
-    case F16_V_K64_S2_E8: return launch_impl<128, 64, 2, 8, TS>(a, b, c, g, sms, s);
-    case F16_V_K32_S6_E4: return launch_impl<128, 32, 6, 4, TS>(a, b, c, g, sms, s);
-    default:             return launch_impl<128, 32, 4, 8, TS>(a, b, c, g, sms, s);
+    case F16_V_N64:       return launch_impl<64, 64, 4, 4, 0>(a, b, c, g, sms, s);
+    case F16_V_K64_S3:    return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
+    case F16_V_K32_S4_E8: return launch_impl<128, 32, 4, 8, 0>(a, b, c, g, sms, s);
+    case F16_V_K64_S2_E8: return launch_impl<128, 64, 2, 8, 0>(a, b, c, g, sms, s);
+    case F16_V_K32_S6_E4: return launch_impl<128, 32, 6, 4, 0>(a, b, c, g, sms, s);
+    case F16_V_K64_S3_DIRECT: return launch_impl<128, 64, 3, 4, 1>(a, b, c, g, sms, s);
+    case F16_V_K64_S3_DIRECT_E8: return launch_impl<128, 64, 3, 8, 1>(a, b, c, g, sms, s);
+    default:              return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
   }
 }
 
@@ -295,10 +318,9 @@ cudaError_t dispatch(int variant, const CUtensorMap& a, const CUtensorMap& b, co
 int gemm_f16_block_n(int variant) { return variant == F16_V_N64 ? 64 : 128; }
 
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                            const GemmF16Args& args, int variant, bool tma_store, int num_sms,
+                            const GemmF16Args& args, int variant, int epi, int num_sms,
                             cudaStream_t stream) {
-  return tma_store ? dispatch<true>(variant, tmA, tmB, tmC, args, num_sms, stream)
-                   : dispatch<false>(variant, tmA, tmB, tmC, args, num_sms, stream);
+  return dispatch(variant, epi, tmA, tmB, tmC, args, num_sms, stream);
 }
 
 int gemm_f16_block_k(int variant) {

@@ -11,6 +11,7 @@ struct GemmF16Args {
   int K16;
   int tiles_m, tiles_n, num_tiles, num_kb;
   float* out;  // used by the masked-store epilogue (N % 4 != 0)
+  int debug;   // ablation (TCBF_DEBUG): bit0 skip output stores, bit1 skip MMAs
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
@@ -20,12 +21,14 @@ enum {
   F16_V_K64_S2_E8 = 2,  // 128x128, BK 64, 2 stages, 8 epilogue warps
   F16_V_K32_S6_E4 = 3,  // 128x128, BK 32, 6 stages, 4 epilogue warps
   F16_V_N64 = 4,        // 128x64,  BK 64, 4 stages, 4 epilogue warps (small N)
-  F16_V_COUNT = 5
+  F16_V_K64_S3_DIRECT = 5,     // 128x128, BK 64, 3 stages, 4 epilogue warps, direct 256-bit stores
+  F16_V_K64_S3_DIRECT_E8 = 6,  // same with 8 epilogue warps
+  F16_V_COUNT = 7
 };
 int gemm_f16_block_n(int variant);
 int gemm_f16_block_k(int variant);
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                            const GemmF16Args& args, int variant, bool tma_store, int num_sms,
+                            const GemmF16Args& args, int variant, int epi, int num_sms,
                             cudaStream_t stream);
 
 struct GemmB1Args {

@@ -153,7 +153,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   p->w_bytes = wb; p->x_bytes = xb; p->out_bytes = ob;
   p->n_packed = (N + 7) / 8 * 8;
   // fp16 kernel variant: 128x64 tiles when N <= 64, else 128x128 (BK 32, 4 stages, 8 epilogue warps)
-  p->f16_variant = N <= 64 ? tcbf::F16_V_N64 : tcbf::F16_V_K32_S4_E8;
+  p->f16_variant = N <= 64 ? tcbf::F16_V_N64 : tcbf::F16_V_K64_S3;
   if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
@@ -188,12 +188,13 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
-  static const char* names[2][tcbf::F16_V_COUNT] = {
-      {"f16_tcgen05_128x128_k32s4e8_stg", "f16_tcgen05_128x128_k64s3e4_stg", "f16_tcgen05_128x128_k64s2e8_stg",
-       "f16_tcgen05_128x128_k32s6e4_stg", "f16_tcgen05_128x64_k64s4e4_stg"},
-      {"f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
-       "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma"}};
-  return names[plan->N % 4 == 0 ? 1 : 0][plan->f16_variant];
+  static const char* names[tcbf::F16_V_COUNT] = {
+      "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
+      "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma", "f16_tcgen05_128x128_k64s3e4_stg256",
+      "f16_tcgen05_128x128_k64s3e8_stg256"};
+  if (plan->N % 8 != 0 && plan->N % 4 != 0) return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked"
+                                                                                      : "f16_tcgen05_128x128_masked";
+  return names[plan->f16_variant];
 }
 
 tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src, tcbf_src_layout layout,
@@ -231,10 +232,22 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (plan->prec == TCBF_PREC_F16) {
-    const int var = plan->f16_variant;
+    // Final kernel choice first, so the tensor-map boxes always match the instantiation:
+    // TMA bulk store needs N % 4 == 0 (16-B row stride), direct 256-bit stores N % 8 == 0,
+    // otherwise the masked-store epilogue (instantiated for the N64 and K64_S3 tiles only).
+    int var = plan->f16_variant;
+    const bool direct = var == tcbf::F16_V_K64_S3_DIRECT || var == tcbf::F16_V_K64_S3_DIRECT_E8;
+    int epi = direct ? 1 : 0;
+    if (plan->N % 4 != 0) {
+      epi = 2;
+      if (var != tcbf::F16_V_N64) var = tcbf::F16_V_K64_S3;
+    } else if (direct && plan->N % 8 != 0) {
+      epi = 0;
+      var = tcbf::F16_V_K64_S3;
+    }
     const int bn = tcbf::gemm_f16_block_n(var);
     const int bk = tcbf::gemm_f16_block_k(var);
-    const bool tma_store = (plan->N % 4) == 0;
+    const bool tma_store = epi == 0;
     CUtensorMap ta, tb, tc;
     // A (weights, K-major [2B][M][K16]): box {BK, 128}, swizzle = BK * 2 bytes
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
@@ -261,7 +274,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.num_tiles = (int)nt;
     a.num_kb = (int)(plan->kp / bk);
     a.out = static_cast<float*>(out);
-    e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, tma_store, plan->num_sms, st);
+    a.debug = 0;
+    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
+    e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, epi, plan->num_sms, st);
   } else {
     tcbf::GemmB1Args a;
     a.w = static_cast<const uint32_t*>(w_packed);

@@ -125,8 +125,16 @@ F16_SHAPES = [
 ]
 
 
+@pytest.fixture(params=["default", "0", "5"])
+def f16_variant(request, monkeypatch):
+    """fp16 kernel variants: default table choice, BK32/8-warp TMA-store, direct 256-bit stores."""
+    if request.param != "default":
+        monkeypatch.setenv("TCBF_F16_VARIANT", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("shape", F16_SHAPES)
-def test_f16_beamform_vs_oracle(tcbf, shape):
+def test_f16_beamform_vs_oracle(tcbf, shape, f16_variant):
     M, N, K, B = shape
     w = synth.generate("uniform", 21, 0, B, M, K)
     x = synth.generate("uniform", 21, 1, B, K, N)
