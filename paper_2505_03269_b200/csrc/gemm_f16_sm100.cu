@@ -315,7 +315,9 @@ cudaError_t dispatch(int variant, int epi, const CUtensorMap& a, const CUtensorM
 
 }  // namespace
 
-int gemm_f16_block_n(int variant) { return variant == F16_V_N64 ? 64 : 128; }
+int gemm_f16_block_n(int variant) {
+  return variant == F16_V_N64 ? 64 : (variant == F16_V_2CTA_N256 ? 256 : 128);
+}
 
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                             const GemmF16Args& args, int variant, int epi, int num_sms,

@@ -23,9 +23,13 @@ enum {
   F16_V_N64 = 4,        // 128x64,  BK 64, 4 stages, 4 epilogue warps (small N)
   F16_V_K64_S3_DIRECT = 5,     // 128x128, BK 64, 3 stages, 4 epilogue warps, direct 256-bit stores
   F16_V_K64_S3_DIRECT_E8 = 6,  // same with 8 epilogue warps
-  F16_V_COUNT = 7
+  F16_V_2CTA_N128 = 7,  // CTA pair, 256x128 tile, BK 64, 4 stages, double-buffered TMEM
+  F16_V_2CTA_N256 = 8,  // CTA pair, 256x256 tile, BK 64, 3 stages, single TMEM buffer
+  F16_V_COUNT = 9
 };
 int gemm_f16_block_n(int variant);
+cudaError_t launch_gemm_f16_2cta(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                 const GemmF16Args& args, int block_n, int num_sms, cudaStream_t stream);
 int gemm_f16_block_k(int variant);
 cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
                             const GemmF16Args& args, int variant, int epi, int num_sms,

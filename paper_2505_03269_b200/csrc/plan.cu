@@ -153,7 +153,11 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   p->w_bytes = wb; p->x_bytes = xb; p->out_bytes = ob;
   p->n_packed = (N + 7) / 8 * 8;
   // fp16 kernel variant: 128x64 tiles when N <= 64, else 128x128 (BK 32, 4 stages, 8 epilogue warps)
-  p->f16_variant = N <= 64 ? tcbf::F16_V_N64 : tcbf::F16_V_K64_S3;
+  // CTA pairs (cta_group::2) halve the per-SM shared-memory traffic of the B operand; used when
+  // M spans more than one 128-row tile.  256-wide tiles when K is long (compute-bound shapes).
+  if (N <= 64) p->f16_variant = tcbf::F16_V_N64;
+  else if (M <= 128 || N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
+  else p->f16_variant = K >= 2048 ? tcbf::F16_V_2CTA_N128 : tcbf::F16_V_K64_S3;
   if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
@@ -191,7 +195,7 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   static const char* names[tcbf::F16_V_COUNT] = {
       "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
       "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma", "f16_tcgen05_128x128_k64s3e4_stg256",
-      "f16_tcgen05_128x128_k64s3e8_stg256"};
+      "f16_tcgen05_128x128_k64s3e8_stg256", "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma"};
   if (plan->N % 8 != 0 && plan->N % 4 != 0) return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked"
                                                                                       : "f16_tcgen05_128x128_masked";
   return names[plan->f16_variant];
@@ -267,7 +271,8 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     }
     tcbf::GemmF16Args a;
     a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
-    a.tiles_m = (int)((plan->M + 127) / 128);
+    const bool use_pair = var == tcbf::F16_V_2CTA_N128 || var == tcbf::F16_V_2CTA_N256;
+    a.tiles_m = (int)((plan->M + (use_pair ? 255 : 127)) / (use_pair ? 256 : 128));
     a.tiles_n = (int)((plan->N + bn - 1) / bn);
     const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
     if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
@@ -276,7 +281,10 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.out = static_cast<float*>(out);
     a.debug = 0;
     if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
-    e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, epi, plan->num_sms, st);
+    if (use_pair)
+      e = tcbf::launch_gemm_f16_2cta(ta, tb, tc, a, bn, plan->num_sms, st);
+    else
+      e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, epi, plan->num_sms, st);
   } else {
     tcbf::GemmB1Args a;
     a.w = static_cast<const uint32_t*>(w_packed);
