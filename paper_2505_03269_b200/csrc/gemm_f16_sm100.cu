@@ -38,8 +38,10 @@ struct F16Cfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int EPI_BUFS = 2;
   // EPI: 0 = swizzled smem staging + TMA bulk store, 1 = direct 256-bit st.global from
-  // registers (no smem traffic; needs N % 8 == 0), 2 = masked scalar stores (any N)
-  static constexpr int EPI_BYTES = EPI == 0 ? EPI_WARPS * EPI_BUFS * 4096 : 0;
+  // registers (no smem traffic; needs N % 8 == 0), 2 = masked scalar stores (any N),
+  // 3 = swizzled smem staging + coalesced 128-bit st.global (4 full lines per warp store,
+  //     keeps the per-SM TMA engine free for the operand loads; needs N % 4 == 0)
+  static constexpr int EPI_BYTES = (EPI == 0 || EPI == 3) ? EPI_WARPS * EPI_BUFS * 4096 : 0;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x (D_r, D_i)
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
@@ -242,6 +244,29 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
             bulk_commit_group();
           }
           sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
+        } else if constexpr (EPI == 3) {
+          uint8_t* buf = stg + sbuf * 4096;
+          __syncwarp();  // previous readers of this buffer are done
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pos = j ^ (lane & 7);
+            *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
+                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+          }
+          __syncwarp();
+          const int rsub = lane >> 3, cj = lane & 7;  // 4 rows x 8 16-byte chunks per instruction
+          const int nb = n0 + c * 32 + cj * 4;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + rsub;
+            const uint4 val = *reinterpret_cast<const uint4*>(buf + rr * 128 + ((cj ^ (rr & 7)) << 4));
+            const int m = m0 + q * 32 + rr;
+            if (m < args.M && nb < args.N) {
+              float* dst = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
+              __stcs(reinterpret_cast<uint4*>(dst), val);  // streaming: written once, never re-read here
+            }
+          }
+          sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
         } else if constexpr (EPI == 1) {
           const int m = m0 + q * 32 + lane;
           const int nb = n0 + c * 32;
@@ -309,6 +334,8 @@ cudaError_t dispatch(int variant, int epi, const CUtensorMap& a, const CUtensorM
     case F16_V_K32_S6_E4: return launch_impl<128, 32, 6, 4, 0>(a, b, c, g, sms, s);
     case F16_V_K64_S3_DIRECT: return launch_impl<128, 64, 3, 4, 1>(a, b, c, g, sms, s);
     case F16_V_K64_S3_DIRECT_E8: return launch_impl<128, 64, 3, 8, 1>(a, b, c, g, sms, s);
+    case F16_V_K64_S3_STG: return launch_impl<128, 64, 3, 4, 3>(a, b, c, g, sms, s);
+    case F16_V_K64_S3_STG_E8: return launch_impl<128, 64, 2, 8, 3>(a, b, c, g, sms, s);
     default:              return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
   }
 }

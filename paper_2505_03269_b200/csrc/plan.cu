@@ -195,7 +195,8 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   static const char* names[tcbf::F16_V_COUNT] = {
       "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
       "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma", "f16_tcgen05_128x128_k64s3e4_stg256",
-      "f16_tcgen05_128x128_k64s3e8_stg256", "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma"};
+      "f16_tcgen05_128x128_k64s3e8_stg256", "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma",
+      "f16_tcgen05_128x128_k64s3e4_stgco", "f16_tcgen05_128x128_k64s2e8_stgco"};
   if (plan->N % 8 != 0 && plan->N % 4 != 0) return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked"
                                                                                       : "f16_tcgen05_128x128_masked";
   return names[plan->f16_variant];
@@ -241,7 +242,8 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     // otherwise the masked-store epilogue (instantiated for the N64 and K64_S3 tiles only).
     int var = plan->f16_variant;
     const bool direct = var == tcbf::F16_V_K64_S3_DIRECT || var == tcbf::F16_V_K64_S3_DIRECT_E8;
-    int epi = direct ? 1 : 0;
+    const bool stgco = var == tcbf::F16_V_K64_S3_STG || var == tcbf::F16_V_K64_S3_STG_E8;
+    int epi = direct ? 1 : (stgco ? 3 : 0);
     if (plan->N % 4 != 0) {
       epi = 2;
       if (var != tcbf::F16_V_N64) var = tcbf::F16_V_K64_S3;
