@@ -22,9 +22,10 @@
 //
 // Roles (persistent CTA per SM, 416 threads):
 //   warp 0      TMEM allocator + single-thread MMA issuer (4 MMAs per K=32 step)
-//   warps 1-4   epilogue: row/column popcounts, tcgen05.ld, correction, TMA store of int32
-//   warps 5-8   expanders for A_r, A_i (one weight row per thread)
-//   warps 9-12  expanders for B_r, B_i, ~B_i (one data column per thread)
+//   warps 1-4   epilogue: tcgen05.ld, single-AND correction, TMA store of int32
+//   warps 5-8   expanders for A_r, A_i (one weight row per thread; also |A_r| + |A_i|)
+//   warps 9-12  expanders for B_r, B_i, ~B_i (one data column per thread; also |B_r|, |B_i|)
+// The popcounts travel expanders -> epilogue through smem with their own full/empty mbarriers.
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -42,7 +43,7 @@ constexpr int TILE_BYTES = 128 * 128;  // one expanded operand tile (rows x 128 
 constexpr int STAGES = 2;
 constexpr int STAGE_BYTES = 5 * TILE_BYTES;  // A_r, A_i, B_r, B_i, ~B_i
 constexpr int EPI_BYTES = 4 * 2 * 4096;
-constexpr int COLSUM_BYTES = 2 * 2 * BN * 4;
+constexpr int COLSUM_BYTES = 2 * 3 * 128 * 4;  // [2 acc buf][|A_r|+|A_i| rows, |B_r|, |B_i| cols][128]
 constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES + COLSUM_BYTES;
 constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
 constexpr int NUM_THREADS = 13 * 32;
@@ -73,20 +74,6 @@ __device__ __forceinline__ void expand_word_pair(uint8_t* base, uint8_t* base_c,
   *reinterpret_cast<uint4*>(base_c + p1) = make_uint4(c1.x ^ m, c1.y ^ m, c1.z ^ m, c1.w ^ m);
 }
 
-__device__ __forceinline__ int popc_row(const uint32_t* __restrict__ row, int Kw) {
-  int s = 0;
-  const uint4* r4 = reinterpret_cast<const uint4*>(row);
-  for (int i = 0; i < Kw / 4; ++i) {
-    uint4 v = __ldg(r4 + i);
-    s += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-  }
-  return s;
-}
-
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
 template <bool TMA_STORE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cgemm_b1_tc_kernel(const __grid_constant__ CUtensorMap tmC, GemmB1Args p, int tiles_m, int tiles_n,
@@ -99,7 +86,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* sfull_bar = tempty_bar + 2;   // popcount sums of a tile written (256 expanders)
+  uint64_t* sempty_bar = sfull_bar + 2;   // popcount sums consumed (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty_bar + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -114,6 +103,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 4);
+      mbar_init(&sfull_bar[s], NUM_EXPANDERS);
+      mbar_init(&sempty_bar[s], 4);
     }
     fence_barrier_init();
     if (TMA_STORE) tma_prefetch_desc(&tmC);
@@ -158,6 +149,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t br = smem_desc_k128(sBr, off), bi = smem_desc_k128(sBi, off);
             const uint64_t bc = smem_desc_k128(sBc, off);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
+            if (p.debug & 2) continue;
             mma_i8_ss(d_re, ar, br, IDESC, acc);  // P(A_r & B_r)
             mma_i8_ss(d_re, ai, bc, IDESC, 1u);   // P(A_i & ~B_i)
             mma_i8_ss(d_im, ar, bi, IDESC, acc);  // P(A_r & B_i)
@@ -183,27 +175,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int m0 = (r / tiles_n) * BM;
       const int n0 = (r % tiles_n) * BN;
       const int cb = it & 1;
-      // popcounts |B_r|, |B_i| of this tile's columns and |A_r|, |A_i| of this thread's row
-      {
-        const int n = n0 + te;
-        int pr = 0, pi = 0;
-        if (n < p.N) {
-          pr = popc_row(p.x + ((size_t)(2 * b) * p.N + n) * p.Kw, p.Kw);
-          pi = popc_row(p.x + ((size_t)(2 * b + 1) * p.N + n) * p.Kw, p.Kw);
-        }
-        colsum[(cb * 2 + 0) * BN + te] = pr;
-        colsum[(cb * 2 + 1) * BN + te] = pi;
-      }
+      // popcounts |A_r|+|A_i| (rows) and |B_r|, |B_i| (columns), accumulated by the expanders
+      mbar_wait(&sfull_bar[cb], (it >> 1) & 1);
       const int m = m0 + q * 32 + lane;
-      int ra = 0;
-      if (m < p.M) {
-        ra = popc_row(p.w + ((size_t)(2 * b) * p.M + m) * p.Kw, p.Kw) +
-             popc_row(p.w + ((size_t)(2 * b + 1) * p.M + m) * p.Kw, p.Kw);
-      }
-      named_bar_sync(1, 128);
-      const int* csr = colsum + (cb * 2 + 0) * BN;
-      const int* csi = colsum + (cb * 2 + 1) * BN;
-
+      const int ra = colsum[(cb * 3 + 0) * 128 + q * 32 + lane];
+      const int* csr = colsum + (cb * 3 + 1) * 128;
+      const int* csi = colsum + (cb * 3 + 2) * 128;
       const int abuf = it & 1;
       mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
       tc_fence_after();
@@ -220,14 +197,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
+        int crv[32], civ[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) { crv[j] = csr[c * 32 + j]; civ[j] = csi[c * 32 + j]; }
+        if (ch == 2 * CHUNKS - 1) {  // last read of this tile's sums
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sempty_bar[cb]);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int cr = csr[c * 32 + j], ci = csi[c * 32 + j];
+          const int cr = crv[j], ci = civ[j];
           const int acc = (int)v[j];
           const int val = part == 0 ? 4 * acc - 2 * ra - 2 * cr + 2 * ci
                                     : 4 * acc - 2 * (ra + cr + ci) + 2 * p.K;
           v[j] = (uint32_t)val;
         }
+        if (p.debug & 1) continue;
         if constexpr (TMA_STORE) {
           if (lane == 0) bulk_wait_group_read<1>();
           __syncwarp();
@@ -268,11 +253,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row = a_side ? e : e - 128;
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int b = t / tiles_per_batch;
       const int r = t - b * tiles_per_batch;
       const int m0 = (r / tiles_n) * BM;
       const int n0 = (r % tiles_n) * BN;
+      int pc_r = 0, pc_i = 0;  // popcounts of this row / column (real, imaginary plane)
       const uint4* src_r;
       const uint4* src_i;
       bool valid;
@@ -294,9 +281,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           nr = valid ? __ldg(src_r + kb + 1) : zero;
           ni = valid ? __ldg(src_i + kb + 1) : zero;
         }
+        pc_r += __popc(wr.x) + __popc(wr.y) + __popc(wr.z) + __popc(wr.w);
+        pc_i += __popc(wi.x) + __popc(wi.y) + __popc(wi.z) + __popc(wi.w);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* st = smem + stage * STAGE_BYTES;
-        if (a_side) {
+        if (p.debug & 4) {
+        } else if (a_side) {
           uint8_t* ar = st + row * 128;
           uint8_t* ai = st + TILE_BYTES + row * 128;
           expand_word(ar, row, 0, wr.x); expand_word(ar, row, 1, wr.y);
@@ -316,6 +306,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_arrive(&full_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      // publish this tile's popcounts for the epilogue's single-AND correction (R1b)
+      const int cb = it & 1;
+      mbar_wait(&sempty_bar[cb], ((it >> 1) & 1) ^ 1);
+      if (a_side) {
+        colsum[(cb * 3 + 0) * 128 + row] = pc_r + pc_i;
+      } else {
+        colsum[(cb * 3 + 1) * 128 + row] = pc_r;
+        colsum[(cb * 3 + 2) * 128 + row] = pc_i;
+      }
+      mbar_arrive(&sfull_bar[cb]);
     }
   }
 

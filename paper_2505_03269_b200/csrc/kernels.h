@@ -42,6 +42,7 @@ struct GemmB1Args {
   const uint32_t* x;  // [B][2][N][Kw]
   int32_t* out;       // [B][2][M][N]
   int M, N, K, Kw, B;
+  int debug;  // ablation (TCBF_DEBUG): bit0 skip stores, bit1 skip MMAs, bit2 skip expansion
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,

@@ -293,6 +293,8 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.x = static_cast<const uint32_t*>(x_packed);
     a.out = static_cast<int32_t*>(out);
     a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
+    a.debug = 0;
+    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
     if (plan->b1_tc) {
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;
