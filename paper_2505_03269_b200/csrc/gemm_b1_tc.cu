@@ -5,12 +5,12 @@
 // IMMA.16832.U8 + LOP3 masks per m16n8k256 (cuobjdump -sass; profiles/).  This kernel keeps
 // HBM traffic at one bit per component and feeds the 5th-generation tensor cores instead:
 //
-//   * the packed words are expanded IN SHARED MEMORY to unsigned bytes u in {0, 1} by bit-plane
-//     masking, byte i of plane j = bit (8i + j) of the word: (w >> j) & 0x01010101.  This is a
-//     fixed permutation of the 32 K-elements of a word, applied identically to both operands,
-//     so every dot product is unchanged;
-//   * tcgen05.mma.kind::i8 (unsigned, int32 accumulate in TMEM) then computes AND-popcounts
-//     P(A & B) = sum_k u_a u_b exactly (PAPER.md:265-270 AND form);
+//   * the packed words are expanded IN SHARED MEMORY to unsigned bytes 2u, u in {0, 1}, by
+//     bit-plane masking, byte i of plane j = 2 * bit (8i + j) of the word.  This is a fixed
+//     permutation of the 32 K-elements of a word, applied identically to both operands, so
+//     every dot product is unchanged;
+//   * tcgen05.mma.kind::i8 (unsigned, int32 accumulate in TMEM) then computes scaled
+//     AND-popcounts 4 P(A & B) = sum_k (2u_a)(2u_b) exactly (PAPER.md:265-270 AND form);
 //   * the complex +-1 result follows from the single-AND identities (reading R1b),
 //     with a = 2u - 1 and |X| the popcount of a row/column:
 //         acc_r = P(A_r & B_r) + P(A_i & ~B_i)          acc_i = P(A_r & B_i) + P(A_i & B_r)
@@ -22,7 +22,7 @@
 //
 // Roles (persistent CTA per SM, 416 threads):
 //   warp 0      TMEM allocator + single-thread MMA issuer (4 MMAs per K=32 step)
-//   warps 1-4   epilogue: tcgen05.ld, single-AND correction, TMA store of int32
+//   warps 1-4   epilogue: tcgen05.ld, + row term + column term (one IADD3), TMA store of int32
 //   warps 5-8   expanders for A_r, A_i (one weight row per thread; also |A_r| + |A_i|)
 //   warps 9-12  expanders for B_r, B_i, ~B_i (one data column per thread; also |B_r|, |B_i|)
 // The popcounts travel expanders -> epilogue through smem with their own full/empty mbarriers.
@@ -51,21 +51,31 @@ constexpr int NUM_EXPANDERS = 256;
 constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (acc_r, acc_i) x 128 columns
 static_assert(SMEM_BYTES <= 232448, "smem budget");
 
+// Bit-plane expansion to bytes in {0, 2}: byte i of plane j = 2 * bit (8i + j) of the word.
+// With both operands scaled by 2 the tensor core accumulates 4 * P(A & B) directly.
+__device__ __forceinline__ uint4 planes_lo(uint32_t w) {
+  const uint32_t m = 0x02020202u;
+  return make_uint4((w << 1) & m, w & m, (w >> 1) & m, (w >> 2) & m);
+}
+__device__ __forceinline__ uint4 planes_hi(uint32_t w) {
+  const uint32_t m = 0x02020202u;
+  return make_uint4((w >> 3) & m, (w >> 4) & m, (w >> 5) & m, (w >> 6) & m);
+}
+
 __device__ __forceinline__ void expand_word(uint8_t* row_base, int row, int q, uint32_t w) {
   // word q of the K block -> chunks 2q (planes 0-3) and 2q+1 (planes 4-7), 128-byte swizzle
-  const uint32_t m = 0x01010101u;
-  uint4 c0 = make_uint4(w & m, (w >> 1) & m, (w >> 2) & m, (w >> 3) & m);
-  uint4 c1 = make_uint4((w >> 4) & m, (w >> 5) & m, (w >> 6) & m, (w >> 7) & m);
+  uint4 c0 = planes_lo(w);
+  uint4 c1 = planes_hi(w);
   const int sw = row & 7;
   *reinterpret_cast<uint4*>(row_base + (((2 * q) ^ sw) << 4)) = c0;
   *reinterpret_cast<uint4*>(row_base + (((2 * q + 1) ^ sw) << 4)) = c1;
 }
 
-// expands w and its complement (planes of ~w are planes of w xor 0x01010101)
+// expands w and its complement (planes of ~w are planes of w xor 0x02020202)
 __device__ __forceinline__ void expand_word_pair(uint8_t* base, uint8_t* base_c, int row, int q, uint32_t w) {
-  const uint32_t m = 0x01010101u;
-  uint4 c0 = make_uint4(w & m, (w >> 1) & m, (w >> 2) & m, (w >> 3) & m);
-  uint4 c1 = make_uint4((w >> 4) & m, (w >> 5) & m, (w >> 6) & m, (w >> 7) & m);
+  const uint32_t m = 0x02020202u;
+  uint4 c0 = planes_lo(w);
+  uint4 c1 = planes_hi(w);
   const int sw = row & 7;
   const int p0 = ((2 * q) ^ sw) << 4, p1 = ((2 * q + 1) ^ sw) << 4;
   *reinterpret_cast<uint4*>(base + p0) = c0;
@@ -178,9 +188,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // popcounts |A_r|+|A_i| (rows) and |B_r|, |B_i| (columns), accumulated by the expanders
       mbar_wait(&sfull_bar[cb], (it >> 1) & 1);
       const int m = m0 + q * 32 + lane;
-      const int ra = colsum[(cb * 3 + 0) * 128 + q * 32 + lane];
-      const int* csr = colsum + (cb * 3 + 1) * 128;
-      const int* csi = colsum + (cb * 3 + 2) * 128;
+      const int rterm = colsum[(cb * 3 + 0) * 128 + q * 32 + lane];  // -2 (|A_r| + |A_i|)
+      const int* cterm_re = colsum + (cb * 3 + 1) * 128;           // 2 (|B_i| - |B_r|)
+      const int* cterm_im = colsum + (cb * 3 + 2) * 128;           // 2K - 2 (|B_r| + |B_i|)
       const int abuf = it & 1;
       mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
       tc_fence_after();
@@ -197,21 +207,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
-        int crv[32], civ[32];
+        const int* cterm = (part == 0 ? cterm_re : cterm_im) + c * 32;
+        int ct[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) { crv[j] = csr[c * 32 + j]; civ[j] = csi[c * 32 + j]; }
-        if (ch == 2 * CHUNKS - 1) {  // last read of this tile's sums
+        for (int j = 0; j < 8; ++j) {  // broadcast 128-bit smem loads
+          const int4 t4 = *reinterpret_cast<const int4*>(cterm + 4 * j);
+          ct[4 * j] = t4.x; ct[4 * j + 1] = t4.y; ct[4 * j + 2] = t4.z; ct[4 * j + 3] = t4.w;
+        }
+        if (ch == 2 * CHUNKS - 1) {  // last read of this tile's correction terms
           __syncwarp();
           if (lane == 0) mbar_arrive(&sempty_bar[cb]);
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int cr = crv[j], ci = civ[j];
-          const int acc = (int)v[j];
-          const int val = part == 0 ? 4 * acc - 2 * ra - 2 * cr + 2 * ci
-                                    : 4 * acc - 2 * (ra + cr + ci) + 2 * p.K;
-          v[j] = (uint32_t)val;
-        }
+        for (int j = 0; j < 32; ++j) v[j] = (uint32_t)((int)v[j] + ct[j] + rterm);  // Re / Im, R1b
         if (p.debug & 1) continue;
         if constexpr (TMA_STORE) {
           if (lane == 0) bulk_wait_group_read<1>();
@@ -310,10 +318,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int cb = it & 1;
       mbar_wait(&sempty_bar[cb], ((it >> 1) & 1) ^ 1);
       if (a_side) {
-        colsum[(cb * 3 + 0) * 128 + row] = pc_r + pc_i;
+        colsum[(cb * 3 + 0) * 128 + row] = -2 * (pc_r + pc_i);
       } else {
-        colsum[(cb * 3 + 1) * 128 + row] = pc_r;
-        colsum[(cb * 3 + 2) * 128 + row] = pc_i;
+        colsum[(cb * 3 + 1) * 128 + row] = 2 * (pc_i - pc_r);
+        colsum[(cb * 3 + 2) * 128 + row] = 2 * p.K - 2 * (pc_r + pc_i);
       }
       mbar_arrive(&sfull_bar[cb]);
     }
