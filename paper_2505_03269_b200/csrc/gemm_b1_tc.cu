@@ -48,6 +48,7 @@ constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES + COLSUM_BYTES;
 constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
 constexpr int NUM_THREADS = 13 * 32;
 constexpr int NUM_EXPANDERS = 256;
+constexpr int EXPANDER_WARPS = NUM_EXPANDERS / 32;  // barrier arrivals are aggregated per warp
 constexpr uint32_t TMEM_COLS = 512;  // 2 buffers x (acc_r, acc_i) x 128 columns
 static_assert(SMEM_BYTES <= 232448, "smem budget");
 
@@ -107,13 +108,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], NUM_EXPANDERS);
+      mbar_init(&full_bar[s], EXPANDER_WARPS);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 4);
-      mbar_init(&sfull_bar[s], NUM_EXPANDERS);
+      mbar_init(&sfull_bar[s], EXPANDER_WARPS);
       mbar_init(&sempty_bar[s], 4);
     }
     fence_barrier_init();
@@ -195,18 +196,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
       tc_fence_after();
       constexpr int CHUNKS = BN / 32;
-#pragma unroll 1
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN;
+      uint32_t vbuf[2][32];
+      tmem_ld_32x32b_x32(tbase, vbuf[0]);
+#pragma unroll
       for (int ch = 0; ch < 2 * CHUNKS; ++ch) {
         const int part = ch / CHUNKS;
         const int c = ch % CHUNKS;
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN + part * BN + c * 32, v);
         tmem_wait_ld();
-        if (ch == 2 * CHUNKS - 1) {
+        if (ch + 1 < 2 * CHUNKS) {
+          tmem_ld_32x32b_x32(tbase + (ch + 1) * 32, vbuf[(ch + 1) & 1]);
+        } else {  // all TMEM reads of this tile done: release the accumulator buffer
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
+        uint32_t* v = vbuf[ch & 1];
         const int* cterm = (part == 0 ? cterm_re : cterm_im) + c * 32;
         int ct[32];
 #pragma unroll
@@ -262,32 +267,46 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    // row pointers of this thread's operand row/column for tile t (nullptr when out of range)
+    auto row_ptrs = [&](int t, const uint4*& pr, const uint4*& pi) {
       const int b = t / tiles_per_batch;
       const int r = t - b * tiles_per_batch;
-      const int m0 = (r / tiles_n) * BM;
-      const int n0 = (r % tiles_n) * BN;
-      int pc_r = 0, pc_i = 0;  // popcounts of this row / column (real, imaginary plane)
-      const uint4* src_r;
-      const uint4* src_i;
-      bool valid;
+      pr = pi = nullptr;
       if (a_side) {
-        valid = (m0 + row) < p.M;
-        src_r = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b) * p.M + m0 + row) * p.Kw);
-        src_i = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b + 1) * p.M + m0 + row) * p.Kw);
+        const int m = (r / tiles_n) * BM + row;
+        if (m < p.M) {
+          pr = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b) * p.M + m) * p.Kw);
+          pi = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b + 1) * p.M + m) * p.Kw);
+        }
       } else {
-        valid = (n0 + row) < p.N;
-        src_r = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b) * p.N + n0 + row) * p.Kw);
-        src_i = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b + 1) * p.N + n0 + row) * p.Kw);
+        const int n = (r % tiles_n) * BN + row;
+        if (n < p.N) {
+          pr = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b) * p.N + n) * p.Kw);
+          pi = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b + 1) * p.N + n) * p.Kw);
+        }
       }
-      const uint4 zero = make_uint4(0, 0, 0, 0);
-      uint4 nr = valid ? __ldg(src_r) : zero;
-      uint4 ni = valid ? __ldg(src_i) : zero;
+    };
+    const uint4* src_r;
+    const uint4* src_i;
+    row_ptrs(blockIdx.x, src_r, src_i);
+    uint4 nr = (blockIdx.x < (unsigned)num_tiles && src_r) ? __ldg(src_r) : zero;
+    uint4 ni = (blockIdx.x < (unsigned)num_tiles && src_i) ? __ldg(src_i) : zero;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int pc_r = 0, pc_i = 0;  // popcounts of this row / column (real, imaginary plane)
+      const bool valid = src_r != nullptr;
+      const uint4* next_r = nullptr;
+      const uint4* next_i = nullptr;
+      const int tn = t + gridDim.x;
+      if (tn < num_tiles) row_ptrs(tn, next_r, next_i);
       for (int kb = 0; kb < num_kb; ++kb) {
         const uint4 wr = nr, wi = ni;
         if (kb + 1 < num_kb) {
           nr = valid ? __ldg(src_r + kb + 1) : zero;
           ni = valid ? __ldg(src_i + kb + 1) : zero;
+        } else {  // first K block of this thread's next tile
+          nr = next_r ? __ldg(next_r) : zero;
+          ni = next_i ? __ldg(next_i) : zero;
         }
         pc_r += __popc(wr.x) + __popc(wr.y) + __popc(wr.z) + __popc(wr.w);
         pc_i += __popc(wi.x) + __popc(wi.y) + __popc(wi.z) + __popc(wi.w);
@@ -310,8 +329,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           expand_word_pair(bi, bc, row, 0, wi.x); expand_word_pair(bi, bc, row, 1, wi.y);
           expand_word_pair(bi, bc, row, 2, wi.z); expand_word_pair(bi, bc, row, 3, wi.w);
         }
-        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the tensor core
-        mbar_arrive(&full_bar[stage]);
+        fence_proxy_async_smem();  // each thread's generic-proxy smem writes -> async proxy
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_bar[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       // publish this tile's popcounts for the epilogue's single-AND correction (R1b)
@@ -323,7 +343,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         colsum[(cb * 3 + 1) * 128 + row] = 2 * (pc_i - pc_r);
         colsum[(cb * 3 + 2) * 128 + row] = 2 * p.K - 2 * (pc_r + pc_i);
       }
-      mbar_arrive(&sfull_bar[cb]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfull_bar[cb]);
+      src_r = next_r;
+      src_i = next_i;
     }
   }
 
