@@ -104,28 +104,38 @@ __global__ void pack_b1_rows(const float* __restrict__ src, int64_t B, int64_t M
   }
 }
 
-// data: [B][K][N] -> [B][2][N][Kw]; thread per (n, word), coalesced reads along n.
+// data: [B][K][N] -> [B][2][N][Kw]; one thread per (column n, chunk of 32 words = 1024 k):
+// the 32 k-rows of a word are read with warp-coalesced 256-byte row segments (consecutive n),
+// all 32 loads of a word in flight; the thread's consecutive words of a row merge in L2
+// (the packed output is 1/64 of the bytes read).
 template <int LAYOUT>
-__global__ void __launch_bounds__(256) pack_b1_transpose(const float* __restrict__ src, int64_t B, int64_t K,
+__global__ void __launch_bounds__(128) pack_b1_transpose(const float* __restrict__ src, int64_t B, int64_t K,
                                                          int64_t N, int64_t Kw, uint32_t* __restrict__ dst) {
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   for (int64_t b = blockIdx.z; b < B; b += gridDim.z)
-  for (int64_t kw = blockIdx.y; kw < Kw; kw += gridDim.y) {
-  uint32_t br = 0, bi = 0;
-  const int64_t kbase = kw * 32;
-#pragma unroll 8
-  for (int j = 0; j < 32; ++j) {
-    const int64_t k = kbase + j;
-    if (k < K) {
-      float2 v = load_c<LAYOUT>(src, b, k, n, K, N);
-      br |= (v.x >= 0.f ? 1u : 0u) << j;
-      bi |= (v.y >= 0.f ? 1u : 0u) << j;
+    for (int64_t w0 = (int64_t)blockIdx.y * 32; w0 < Kw; w0 += (int64_t)gridDim.y * 32) {
+      uint32_t* dr = dst + ((b * 2 + 0) * N + n) * Kw + w0;
+      uint32_t* di = dst + ((b * 2 + 1) * N + n) * Kw + w0;
+#pragma unroll 1
+      for (int w = 0; w < 32 && w0 + w < Kw; ++w) {
+        uint32_t br = 0, bi = 0;
+        const int64_t kbase = (w0 + w) * 32;
+        if (kbase < K) {
+          float2 v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (kbase + j < K) ? load_c<LAYOUT>(src, b, kbase + j, n, K, N)
+                                                           : make_float2(-1.f, -1.f);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            br |= (v[j].x >= 0.f ? 1u : 0u) << j;  // NaN -> 0; rows k >= K -> padding bit 0
+            bi |= (v[j].y >= 0.f ? 1u : 0u) << j;
+          }
+        }
+        dr[w] = br;
+        di[w] = bi;
+      }
     }
-  }
-  dst[((b * 2 + 0) * N + n) * Kw + kw] = br;
-  dst[((b * 2 + 1) * N + n) * Kw + kw] = bi;
-  }
 }
 
 inline unsigned grid_for(int64_t work, int threads) {
@@ -164,9 +174,9 @@ cudaError_t launch_pack_b1(const float* src, int layout, int operand, int64_t B,
     if (layout == 0) pack_b1_rows<0><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, Kw, dst);
     else pack_b1_rows<1><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, Kw, dst);
   } else {
-    dim3 grid((unsigned)((C + 255) / 256), (unsigned)cap_dim(Kw), (unsigned)cap_dim(B));
-    if (layout == 0) pack_b1_transpose<0><<<grid, 256, 0, stream>>>(src, B, R, C, Kw, dst);
-    else pack_b1_transpose<1><<<grid, 256, 0, stream>>>(src, B, R, C, Kw, dst);
+    dim3 grid((unsigned)((C + 127) / 128), (unsigned)cap_dim((Kw + 31) / 32), (unsigned)cap_dim(B));
+    if (layout == 0) pack_b1_transpose<0><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst);
+    else pack_b1_transpose<1><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst);
   }
   return cudaGetLastError();
 }
