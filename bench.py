@@ -79,28 +79,34 @@ def load_peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
-def roofline_for(c, gemm_ms, peaks, long_step):
-    """Dominant kernel = the beamform GEMM.  f16: tensor peak = measured bf16 peak x 1 (same
-    nominal rate); b1 (popc on CUDA cores): bound 'alu' against the derived POPC peak."""
+def roofline_for(c, gemm_ms, peaks, long_step, variant=""):
+    """Dominant kernel = the beamform GEMM.  Binding roof = the slower of the HBM time
+    (algorithmic bytes / measured copy bandwidth) and the tensor time (useful ops / peak):
+    fp16 tensor peak = measured bf16 peak (same nominal rate); the 1-bit tensor-core kernel
+    runs int8 MMAs whose nominal rate is 2x fp16 (guide ratio) -> 2 x measured bf16.  The
+    CUDA-core popc kernel (TCBF_B1_KERNEL=popc) reports 'alu' against 16 POPC/clk/SM."""
     ops = useful_ops(c)
     byts = gemm_bytes(c)
     bw = peaks["hbm"]
-    if c["prec"] == "f16":
-        tflops = peaks["bf16_sus"] if long_step else peaks["bf16"]
-        ridge = tflops * 1e12 / (bw * 1e9)
-        if ops / byts < ridge:
-            ach = byts / (gemm_ms * 1e-3) / 1e9
-            return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
-                        peak_src=peaks["src"])
-        ach = ops / (gemm_ms * 1e-3) / 1e12
-        return dict(bound="tensor", achieved=round(ach, 1), peak=tflops, unit="TFLOP/s", frac=round(ach / tflops, 4),
-                    peak_src=peaks["src"] + (" sustained" if long_step else " burst"))
-    # 1-bit popc kernel: 4 POPC per complex 32-bit word quadruple -> peak useful ops =
-    # popc_per_clk_per_sm * 148 SMs * clk * 32 bits * 2 (ops per MAC); 16 POPC/clk/SM (DESIGN.md)
-    alu_peak = 16 * 148 * 1.965e9 * 32 * 2 / 1e12
-    ach = ops / (gemm_ms * 1e-3) / 1e12
-    return dict(bound="alu", achieved=round(ach, 1), peak=round(alu_peak, 1), unit="TOP/s",
-                frac=round(ach / alu_peak, 4), peak_src="derived (16 POPC/clk/SM x 148 x 1965 MHz)")
+    t_ms = gemm_ms * 1e-3
+    if c["prec"] == "b1" and "popc" in variant:
+        alu_peak = 16 * 148 * 1.965e9 * 32 * 2 / 1e12
+        ach = ops / t_ms / 1e12
+        return dict(bound="alu", achieved=round(ach, 1), peak=round(alu_peak, 1), unit="TOP/s",
+                    frac=round(ach / alu_peak, 4), peak_src="derived (16 POPC/clk/SM x 148 x 1965 MHz)")
+    ratio = 1.0 if c["prec"] == "f16" else 2.0
+    base = peaks["bf16_sus"] if long_step else peaks["bf16"]
+    tpeak = base * ratio
+    t_hbm = byts / (bw * 1e9)
+    t_tc = ops / (tpeak * 1e12)
+    src = peaks["src"] + (" sustained" if long_step else " burst") + ("" if ratio == 1 else " x2 (int8 nominal ratio)")
+    if t_hbm >= t_tc:
+        ach = byts / t_ms / 1e9
+        return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
+                    peak_src=peaks["src"], tensor_frac=round(ops / t_ms / 1e12 / tpeak, 4))
+    ach = ops / t_ms / 1e12
+    return dict(bound="tensor", achieved=round(ach, 1), peak=round(tpeak, 1), unit="TOP/s" if ratio == 2 else "TFLOP/s",
+                frac=round(ach / tpeak, 4), peak_src=src, hbm_frac=round(byts / t_ms / 1e9 / bw, 4))
 
 
 def traffic_for(c_name, variant):
@@ -323,7 +329,7 @@ def run_tcbf(args, c):
     e2e_val = world * useful_ops(c) / e2e_s / 1e12
 
     peaks = load_peaks()
-    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0))
+    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant)
     roof["traffic"] = traffic_for(args.config, plan.variant)
     roof["kernel"] = plan.variant
     roof["kernel_ms"] = round(gemm_ms_max, 4)

@@ -104,7 +104,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_kb = p.Kw / KB_WORDS;
-  const int tiles_per_batch = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -181,10 +180,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int b = t / tiles_per_batch;
-      const int r = t - b * tiles_per_batch;
-      const int m0 = (r / tiles_n) * BM;
-      const int n0 = (r % tiles_n) * BN;
+      int b, mt, nt;
+      tile_coords(t, tiles_m, tiles_n, p.group_m, b, mt, nt);
+      const int m0 = mt * BM;
+      const int n0 = nt * BN;
       const int cb = it & 1;
       // popcounts |A_r|+|A_i| (rows) and |B_r|, |B_i| (columns), accumulated by the expanders
       mbar_wait(&sfull_bar[cb], (it >> 1) & 1);
@@ -270,17 +269,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint4 zero = make_uint4(0, 0, 0, 0);
     // row pointers of this thread's operand row/column for tile t (nullptr when out of range)
     auto row_ptrs = [&](int t, const uint4*& pr, const uint4*& pi) {
-      const int b = t / tiles_per_batch;
-      const int r = t - b * tiles_per_batch;
+      int b, mt, nt;
+      tile_coords(t, tiles_m, tiles_n, p.group_m, b, mt, nt);
       pr = pi = nullptr;
       if (a_side) {
-        const int m = (r / tiles_n) * BM + row;
+        const int m = mt * BM + row;
         if (m < p.M) {
           pr = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b) * p.M + m) * p.Kw);
           pi = reinterpret_cast<const uint4*>(p.w + ((size_t)(2 * b + 1) * p.M + m) * p.Kw);
         }
       } else {
-        const int n = (r % tiles_n) * BN + row;
+        const int n = nt * BN + row;
         if (n < p.N) {
           pr = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b) * p.N + n) * p.Kw);
           pi = reinterpret_cast<const uint4*>(p.x + ((size_t)(2 * b + 1) * p.N + n) * p.Kw);

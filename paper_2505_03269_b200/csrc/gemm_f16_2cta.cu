@@ -6,8 +6,8 @@
 //   * CTA r of the pair TMA-loads its own 128 weight rows (A_r, A_i) and its half of the BN data
 //     columns (B_r, B_i), signalling the leader's full barrier (cp.async.bulk.tensor.cta_group::2);
 //   * the leader's single MMA thread issues tcgen05.mma.cta_group::2 (M=256, N=BN, K=16); the
-//     tensor cores of the pair exchange the B halves, so each SM's shared memory serves only half
-//     of B per MMA -- the shared-memory bandwidth that bounds the 1-CTA kernel;
+//     tensor cores of the pair exchange the B halves, so each SM loads and serves only half of B
+//     per MMA (less TMA, L2 and shared-memory traffic -- and power -- per useful flop);
 //   * commits are multicast to both CTAs' barriers; each CTA drains its own TMEM (its 128 rows x
 //     BN) in the epilogue and arrives remotely on the leader's TMEM-empty barrier.
 // BN = 128 keeps two accumulator sets in TMEM (store-bound radio shapes, epilogue overlapped);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int tiles_n = args.tiles_n;
-  const int tiles_per_batch = args.tiles_m * tiles_n;  // tiles_m counts 256-row pair tiles
+  // tiles_m counts 256-row pair tiles
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -157,10 +157,10 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < args.num_tiles; t += npairs) {
-        const int b = t / tiles_per_batch;
-        const int r = t - b * tiles_per_batch;
-        const int m0 = (r / tiles_n) * 256 + (int)rank * 128;
-        const int n0 = (r % tiles_n) * BN + (int)rank * Cfg::BH;
+        int b, mt, nt;
+        tile_coords(t, args.tiles_m, tiles_n, args.group_m, b, mt, nt);
+        const int m0 = mt * 256 + (int)rank * 128;
+        const int n0 = nt * BN + (int)rank * Cfg::BH;
         for (int kb = 0; kb < args.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           const uint32_t lbar = mapa_shared(&full_bar[stage], 0);
@@ -228,10 +228,10 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
     int it = 0;
     const uint32_t tempty_leader[2] = {mapa_shared(&tempty_bar[0], 0), mapa_shared(&tempty_bar[1], 0)};
     for (int t = pair; t < args.num_tiles; t += npairs, ++it) {
-      const int b = t / tiles_per_batch;
-      const int r = t - b * tiles_per_batch;
-      const int m0 = (r / tiles_n) * 256 + (int)rank * 128;
-      const int n0 = (r % tiles_n) * BN;
+      int b, mt, nt;
+      tile_coords(t, args.tiles_m, tiles_n, args.group_m, b, mt, nt);
+      const int m0 = mt * 256 + (int)rank * 128;
+      const int n0 = nt * BN;
       const int abuf = Cfg::ACC_BUFS == 2 ? (it & 1) : 0;
       const uint32_t aphase = Cfg::ACC_BUFS == 2 ? ((it >> 1) & 1) : (it & 1);
       mbar_wait(&tfull_bar[abuf], aphase);

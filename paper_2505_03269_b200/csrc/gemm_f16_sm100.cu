@@ -121,7 +121,6 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int tiles_per_batch = args.tiles_m * args.tiles_n;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -129,10 +128,10 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x) {
-        const int b = t / tiles_per_batch;
-        const int r = t - b * tiles_per_batch;
-        const int m0 = (r / args.tiles_n) * BM;
-        const int n0 = (r % args.tiles_n) * BN;
+        int b, mt, nt;
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, b, mt, nt);
+        const int m0 = mt * BM;
+        const int n0 = nt * BN;
         for (int kb = 0; kb < args.num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
@@ -201,10 +200,10 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
     int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < args.num_tiles; t += gridDim.x, ++it) {
-      const int b = t / tiles_per_batch;
-      const int r = t - b * tiles_per_batch;
-      const int m0 = (r / args.tiles_n) * BM;
-      const int n0 = (r % args.tiles_n) * BN;
+      int b, mt, nt;
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, b, mt, nt);
+      const int m0 = mt * BM;
+      const int n0 = nt * BN;
       const int abuf = it & 1;
       mbar_wait(&tfull_bar[abuf], (it >> 1) & 1);
       tc_fence_after();

@@ -12,6 +12,7 @@ struct GemmF16Args {
   int tiles_m, tiles_n, num_tiles, num_kb;
   float* out;  // used by the masked-store epilogue (N % 4 != 0)
   int debug;   // ablation (TCBF_DEBUG): bit0 skip output stores, bit1 skip MMAs
+  int group_m; // tile rows per rasterisation group (tile_coords)
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
@@ -43,6 +44,7 @@ struct GemmB1Args {
   int32_t* out;       // [B][2][M][N]
   int M, N, K, Kw, B;
   int debug;  // ablation (TCBF_DEBUG): bit0 skip stores, bit1 skip MMAs, bit2 skip expansion
+  int group_m;  // tile rows per rasterisation group (tile_coords)
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,

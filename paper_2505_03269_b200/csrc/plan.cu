@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -157,7 +158,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   // M spans more than one 128-row tile.  256-wide tiles when K is long (compute-bound shapes).
   if (N <= 64) p->f16_variant = tcbf::F16_V_N64;
   else if (M <= 128 || N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
-  else p->f16_variant = K >= 2048 ? tcbf::F16_V_2CTA_N128 : tcbf::F16_V_K64_S3;
+  else p->f16_variant = (K >= 2048 && N >= 256) ? tcbf::F16_V_2CTA_N256 : tcbf::F16_V_K64_S3;
   if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
@@ -281,6 +282,12 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.num_tiles = (int)nt;
     a.num_kb = (int)(plan->kp / bk);
     a.out = static_cast<float*>(out);
+    {  // rasterisation group: keep ~48 MB of weight rows (A_r + A_i, K16 fp16) of a group in L2
+      const int64_t rows_per_tile = use_pair ? 256 : 128;
+      const int64_t bytes_per_tile_row = rows_per_tile * plan->kp * 4;
+      int64_t gm = (48ll << 20) / (bytes_per_tile_row > 0 ? bytes_per_tile_row : 1);
+      a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, a.tiles_m));
+    }
     a.debug = 0;
     if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
     if (use_pair)
@@ -295,6 +302,11 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
     a.debug = 0;
     if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
+    {  // rasterisation group: 1-bit operands are small; ~16 MB of packed weight rows per group
+      const int64_t bytes_per_tile_row = 128 * plan->kp * 8;
+      const int64_t tm = (plan->M + 127) / 128;
+      a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bytes_per_tile_row, tm));
+    }
     if (plan->b1_tc) {
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;

@@ -10,6 +10,23 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---------------------------------------------------------------- tile scheduling
+// Batch-major, grouped rasterisation of a batch's tiles_m x tiles_n tile grid: groups of
+// `group_m` tile rows are walked column by column, so the tiles in flight at any time share a
+// compact window of weight rows and data columns that stays resident in L2 (126 MB).
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group_m, int& b, int& mt,
+                                            int& nt) {
+  const int per_batch = tiles_m * tiles_n;
+  b = t / per_batch;
+  const int r = t - b * per_batch;
+  const int per_group = group_m * tiles_n;
+  const int g = r / per_group;
+  const int local = r - g * per_group;
+  const int rows = min(group_m, tiles_m - g * group_m);
+  mt = g * group_m + local % rows;
+  nt = local / rows;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

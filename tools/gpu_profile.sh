@@ -11,7 +11,7 @@ NCU=/usr/local/cuda/bin/ncu
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -s 9 -c 20 --csv \
   --log-file ${OUT}_launches.csv python bench.py --config $CFG --steps 10 --warmup 3 --no-cpu-baseline \
   > ${OUT}_launches_bench.log 2>&1
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cgemm -s 3 -c 1 \
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cgemm -s 4 -c 1 \
   -o ${OUT}_full -f python bench.py --config $CFG --steps 4 --warmup 3 --no-cpu-baseline \
   > ${OUT}_full.log 2>&1
 echo "profile done: $CFG"
