@@ -201,6 +201,7 @@ def oracle_sample(c, seconds, rank_b0=0, budget_rows=None):
 
 
 def cpu_baseline(c, seconds=12.0):
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())   # before liboracle (libgomp) loads
     rate, rows, t = oracle_sample(c, seconds)
     return {"value": round(rate / 1e12, 6), "unit": "TeraOps/s", "cores": os.cpu_count(), "kind": "oracle",
             "sample": f"oracle (C, fp64/int64 triple loop, OpenMP {os.cpu_count()} threads) on beams 0..{rows - 1} "
@@ -212,6 +213,8 @@ def run_reference(args, c):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    # torchrun exports OMP_NUM_THREADS=1; the oracle is timed on all host cores (reported below)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     import numpy as np  # noqa: F401
     budget = max(0.05, min(0.5, 150.0 / max(1, args.steps + args.warmup)))
     rate, rows, t = oracle_sample(c, budget * 4)
@@ -254,9 +257,14 @@ def run_tcbf(args, c):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":   # test mode: every rank on cuda:0 (exercises the N>1 path on 1 GPU)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local)
     sh = weak_shard(c["B"], rank)
     M, N, K, B = c["M"], c["N"], c["K"], c["B"]
@@ -372,6 +380,8 @@ def main():
     ap.add_argument("--config", default="radio_f16", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="tcbf", choices=["tcbf", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo = test mode, all ranks share cuda:0 (production runs use nccl)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
