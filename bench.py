@@ -7,8 +7,10 @@
         --master-port P bench.py --gpus N --steps K --warmup W
 
 A step = one pass of the hot path over one batch of synthetic data resident in HBM:
-tcbf_pack(DATA) (fp32 -> packed operand, §8 a1/a2) + tcbf_beamform (§8 a3-a6).  The
-weights are packed once before timing (PAPER.md:362: the model matrix is prepared once;
+the fp32 data -> packed operand conversion (§8 a1/a2) + the beamform GEMM (§8 a3-a6), i.e.
+tcbf_beamform_raw -- one fused kernel for short-K fp16 plans (each data element converted
+once inside the GEMM), otherwise tcbf_pack(DATA) + tcbf_beamform.  The weights are packed
+once before timing (PAPER.md:362: the model matrix is prepared once;
 PAPER.md:48: weights constant over a period).  Useful ops = 8*B*M*N*K.
 Multi-GPU: weak scaling, every rank beamforms its own `batch` channels (global batch =
 N x batch), no data-path collective; time = max over ranks of CUDA-event time.
@@ -59,12 +61,13 @@ def useful_ops(c):
     return 8.0 * c["M"] * c["N"] * c["K"] * c["B"]
 
 
-def gemm_bytes(c):
+def gemm_bytes(c, fused=False):
     """Algorithmic bytes of one beamform launch (PAPER.md:319 'theoretical amount
-    of bytes'): logical inputs read once, output written once."""
+    of bytes'): logical inputs read once, output written once.  The fused kernel reads the data
+    as fp32 complex (8 B) instead of the packed fp16 operand (4 B)."""
     B, M, N, K = c["B"], c["M"], c["N"], c["K"]
     if c["prec"] == "f16":
-        return B * (4 * M * K + 4 * K * N + 8 * M * N)
+        return B * (4 * M * K + (8 if fused else 4) * K * N + 8 * M * N)
     return B * ((M * K + K * N) / 4.0 + 8 * M * N)
 
 
@@ -79,14 +82,14 @@ def load_peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
-def roofline_for(c, gemm_ms, peaks, long_step, variant=""):
+def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
     """Dominant kernel = the beamform GEMM.  Binding roof = the slower of the HBM time
     (algorithmic bytes / measured copy bandwidth) and the tensor time (useful ops / peak):
     fp16 tensor peak = measured bf16 peak (same nominal rate); the 1-bit tensor-core kernel
     runs int8 MMAs whose nominal rate is 2x fp16 (guide ratio) -> 2 x measured bf16.  The
     CUDA-core popc kernel (TCBF_B1_KERNEL=popc) reports 'alu' against 16 POPC/clk/SM."""
     ops = useful_ops(c)
-    byts = gemm_bytes(c)
+    byts = gemm_bytes(c, fused)
     bw = peaks["hbm"]
     t_ms = gemm_ms * 1e-3
     if c["prec"] == "b1" and "popc" in variant:
@@ -310,8 +313,11 @@ def run_tcbf(args, c):
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
-        plan.beamform(wp, xp, out, stream=stream)
+        if plan.raw_fused:
+            plan.beamform_raw(wp, xsrc, out=out, stream=stream)
+        else:
+            plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
+            plan.beamform(wp, xp, out, stream=stream)
 
     for _ in range(args.warmup):
         if flush:
@@ -325,13 +331,18 @@ def run_tcbf(args, c):
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
+    fused = plan.raw_fused
     for i in range(args.steps):
         if flush:
             flush_buf.fill_(float(i))   # evict L2 between timed steps (not inside the timed spans)
         ev[i][0].record(stream)
-        plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
-        ev[i][1].record(stream)
-        plan.beamform(wp, xp, out, stream=stream)
+        if fused:
+            ev[i][1].record(stream)
+            plan.beamform_raw(wp, xsrc, out=out, stream=stream)
+        else:
+            plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
+            ev[i][1].record(stream)
+            plan.beamform(wp, xp, out, stream=stream)
         ev[i][2].record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -362,11 +373,12 @@ def run_tcbf(args, c):
     e2e_val = world * useful_ops(c) / e2e_s / 1e12
 
     peaks = load_peaks()
-    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant)
+    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
+                        fused=fused)
     roof["traffic"] = traffic_for(args.config, plan.variant)
-    roof["kernel"] = plan.variant
+    roof["kernel"] = "f16_tcgen05_fused_pack_bres_128x128" if fused else plan.variant
     roof["kernel_ms"] = round(gemm_ms_max, 4)
-    roof["algorithmic_bytes_per_launch"] = gemm_bytes(c)
+    roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
     roof["useful_ops_per_launch"] = useful_ops(c)
 
     line = {
@@ -376,7 +388,8 @@ def run_tcbf(args, c):
         "vs_baseline": None, "dtype": c["prec"], "data": "synthetic (seeded counter-based generator, synth/)",
         "config": {"workload": args.config, "desc": c["desc"], "M": M, "N": N, "K": K, "batch_per_gpu": B,
                    "global_batch": B * world, "precision": c["prec"],
-                   "step": "tcbf_pack(data) + tcbf_beamform; weights packed once",
+                   "step": ("tcbf_beamform_raw (data pack fused into the GEMM)" if fused else
+                            "tcbf_pack(data) + tcbf_beamform") + "; weights packed once",
                    "l2": ("flushed between steps (256 MiB write)" if flush else
                           f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
                    "parallelism": f"batch-sharded x{world}, no data-path collective",
@@ -385,7 +398,7 @@ def run_tcbf(args, c):
         "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s", "h2d_bytes_per_step": int(x_host.numel() * 4),
                 "d2h_bytes_per_step": int(plan.out_bytes), "api": "tcbf_beamform_host (pinned host buffers)",
                 "steps": e2e_steps},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": sampler.summary(),
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:

@@ -110,6 +110,16 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
 tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed,
                           void* out, void* stream);
 
+/* The beamformer straight from the fp32 data source (device pointer, `layout` as for
+ * tcbf_pack): the data pack is fused into the GEMM where the shape allows it (F16 plans with
+ * round_up(K, 64) <= 256 and N % 4 == 0: each data element is converted to fp16 once, inside
+ * the GEMM, into a shared-memory-resident operand -- PAPER.md:414 future work, no separate
+ * transpose/pack pass).  Other plans pack into a stream-ordered scratch buffer
+ * (cudaMallocAsync; ALLOC on failure) and call tcbf_beamform.  Results are bit-identical to
+ * tcbf_pack(DATA) followed by tcbf_beamform.  Same pointer rules as tcbf_beamform. */
+tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
+                              tcbf_src_layout layout, void* out, void* stream);
+
 /* End-to-end convenience over HOST buffers (the e2e boundary): copies the fp32
  * data X (host, pinned recommended) to the device in batch chunks, packs it,
  * beamforms against the already packed device weights and copies the output back

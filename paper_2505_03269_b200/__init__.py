@@ -61,6 +61,8 @@ def lib():
         L.tcbf_pack.argtypes = [vp, ctypes.c_int, vp, ctypes.c_int, vp, vp]
         L.tcbf_beamform.restype = ctypes.c_int
         L.tcbf_beamform.argtypes = [vp, vp, vp, vp, vp]
+        L.tcbf_beamform_raw.restype = ctypes.c_int
+        L.tcbf_beamform_raw.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
         L.tcbf_beamform_host.restype = ctypes.c_int
         L.tcbf_beamform_host.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.tcbf_last_launch_count.restype = ctypes.c_int
@@ -158,6 +160,21 @@ class Plan:
                                    ctypes.c_void_p(x_packed.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                    _stream_ptr(stream, w_packed.device)), "tcbf_beamform")
         return out
+
+    def beamform_raw(self, w_packed, x_src, layout="interleaved", out=None, stream=None):
+        """Beamform straight from the fp32 data (pack fused into the GEMM where supported)."""
+        if out is None:
+            out = self.alloc_output(w_packed.device)
+        _check(lib().tcbf_beamform_raw(self._h, ctypes.c_void_p(w_packed.data_ptr()),
+                                       ctypes.c_void_p(x_src.data_ptr()), _LAYOUT[layout],
+                                       ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream, w_packed.device)),
+               "tcbf_beamform_raw")
+        return out
+
+    @property
+    def raw_fused(self) -> bool:
+        """True when beamform_raw runs the fused single-kernel path for this plan."""
+        return self.precision == F16 and self.k_packed <= 256 and self.N % 4 == 0
 
     def beamform_host(self, w_packed_dev, x_host, out_host, layout="interleaved"):
         """End-to-end over host buffers (torch CPU tensors, pinned for overlap)."""

@@ -38,6 +38,10 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
                             const GemmF16Args& args, int variant, int epi, int num_sms,
                             cudaStream_t stream);
 
+bool gemm_f16_fused_supported(int64_t K16, int64_t N);
+cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
+                                  const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
+
 struct GemmB1Args {
   const uint32_t* w;  // [B][2][M][Kw]
   const uint32_t* x;  // [B][2][N][Kw]

@@ -326,6 +326,51 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
   return TCBF_OK;
 }
 
+tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
+                              tcbf_src_layout layout, void* out, void* stream) {
+  g_launches = 0;
+  if (!plan || !w_packed || !x_src || !out) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (layout != TCBF_SRC_INTERLEAVED && layout != TCBF_SRC_PLANAR) return fail(TCBF_ERR_INVALID_ARG, "bad layout");
+  if (!aligned(w_packed, 16) || !aligned(out, 16) || !aligned(x_src, layout == TCBF_SRC_INTERLEAVED ? 8 : 4))
+    return fail(TCBF_ERR_INVALID_ARG, "misaligned pointer");
+  tcbf_status s = check_device(plan);
+  if (s != TCBF_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  bool fused = plan->prec == TCBF_PREC_F16 && tcbf::gemm_f16_fused_supported(plan->kp, plan->N);
+  if (const char* env = getenv("TCBF_NO_FUSED")) fused = fused && atoi(env) == 0;
+  if (fused) {
+    CUtensorMap ta, tc;
+    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + 127) / 128);
+    a.tiles_n = (int)((plan->N + 127) / 128);
+    a.num_kb = (int)(plan->kp / 64);
+    const int64_t nu = (int64_t)a.tiles_n * plan->B;
+    if (nu > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
+    a.num_tiles = (int)(nu * a.tiles_m);
+    a.out = static_cast<float*>(out);
+    cudaError_t e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, plan->x_bytes, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (data scratch)");
+  s = tcbf_pack(plan, TCBF_DATA, x_src, layout, scratch, stream);
+  if (s == TCBF_OK) s = tcbf_beamform(plan, w_packed, scratch, out, stream);
+  cudaFreeAsync(scratch, st);
+  g_launches = s == TCBF_OK ? 2 : 0;
+  return s;
+}
+
 int tcbf_last_launch_count(void) { return g_launches; }
 
 const char* tcbf_status_string(tcbf_status status) {

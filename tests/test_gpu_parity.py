@@ -205,6 +205,63 @@ def test_inputs_unmodified(tcbf):
         assert torch.equal(w, w0) and torch.equal(x, x0) and torch.equal(wp, wp0) and torch.equal(xp, xp0)
 
 
+# ------------------------------------------------------------------ fused fp32 path (tcbf_beamform_raw)
+RAW_SHAPES = [
+    (200, 300, 100, 3, "interleaved"),   # fused, ragged M/N/K, N % 8 != 0 -> scalar loads
+    (256, 256, 256, 2, "interleaved"),   # fused, vector loads, exactly K16 = 256
+    (130, 136, 64, 3, "planar"),         # fused, planar source
+    (8, 64, 32, 2, "interleaved"),       # tiny (BASELINE configs[0])
+    (64, 96, 300, 2, "interleaved"),     # K16 = 320 > 256 -> pack + beamform fallback
+    (70, 77, 40, 2, "interleaved"),      # N % 4 != 0 -> fallback
+]
+
+
+@pytest.mark.parametrize("shape", RAW_SHAPES)
+def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape):
+    M, N, K, B, layout = shape
+    w = synth.generate("phase", 17, 0, B, M, K)
+    x = synth.generate("adc", 17, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
+    xd = _dev(conv(x))
+    y_raw = plan.beamform_raw(wp, xd, layout)
+    y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
+    torch.cuda.synchronize()
+    assert torch.equal(y_raw, y_ref)
+    ref = oracle.cgemm_f16(conv(w), conv(x), 0 if layout == "interleaved" else 1, M, N, K, B)
+    _check_f16(y_raw.cpu().numpy(), ref, w, x)
+
+
+def test_b1_beamform_raw_falls_back_bit_exact(tcbf):
+    M, N, K, B = 70, 45, 300, 2
+    w = synth.generate("adc", 5, 0, B, M, K)
+    x = synth.generate("adc", 5, 1, B, K, N)
+    plan = tcbf.Plan(M, N, K, B, "b1")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(synth.to_interleaved(w)))
+    y = plan.beamform_raw(wp, _dev(synth.to_interleaved(x)))
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x),
+                                                          0, M, N, K, B))
+
+
+def test_full_size_radio_f16_raw_sampled(tcbf):
+    """BASELINE configs[1] through the fused path, as bench.py times it."""
+    M, N, K, B = 1024, 1024, 256, 256
+    seed = synth.SEED_BASE + 1
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    assert plan.raw_fused
+    wp = plan.pack(tcbf.WEIGHTS, synth.generate_device("phase", seed, 0, B, M, K))
+    y = plan.beamform_raw(wp, synth.generate_device("adc", seed, 1, B, K, N))
+    torch.cuda.synchronize()
+    rows = [0, 5, 640, 1023]
+    for b in (0, 77, 255):
+        w = synth.generate("phase", seed, 0, B, M, K, b_sel=[b], r_sel=rows)
+        x = synth.generate("adc", seed, 1, B, K, N, b_sel=[b])
+        ref = oracle.cgemm_f16(synth.to_interleaved(w), synth.to_interleaved(x), 0, len(rows), N, K, 1)
+        _check_f16(y[b][:, rows].cpu().numpy()[None], ref, w, x)
+
+
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
 @pytest.fixture(params=["tc", "popc"])
 def b1_kernel(request, monkeypatch):
