@@ -50,6 +50,10 @@ CONFIGS = {
     "fig3_f16_small": _cfg("f16", 1024, 1024, 64, 256, "uniform", "uniform", 4, "fp16 small 256x1024x1024x64"),
     "fig3_b1_small": _cfg("b1", 1024, 1024, 256, 256, "uniform", "uniform", 4, "int1 small 256x1024x1024x256"),
 }
+# LOFAR station sweep (Fig. 7): 1024 beams, 1024 samples, batch 256, K = 8..512
+for _k in (8, 16, 32, 48, 64, 96, 128, 192, 256, 384, 512):
+    CONFIGS[f"lofar_k{_k}"] = _cfg("f16", 1024, 1024, _k, 256, "phase", "adc", 1,
+                                   f"LOFAR station sweep fp16: M=1024 beams, K={_k} stations, N=1024, batch=256")
 for _n in (1024, 2048, 4096, 8192, 16384):
     CONFIGS[f"square_f16_{_n}"] = _cfg("f16", _n, _n, _n, 1, "uniform", "uniform", 4, f"square fp16 M=N=K={_n}")
     CONFIGS[f"square_b1_{_n}"] = _cfg("b1", _n, _n, _n, 1, "uniform", "uniform", 4, f"square 1-bit M=N=K={_n}")

@@ -120,6 +120,17 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
 tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
                               tcbf_src_layout layout, void* out, void* stream);
 
+/* Steering weights for a far-field plane wave (Eqs. 1-3): writes the plan's fp32
+ * weight source (interleaved [B][M][K] float2 or planar [B][2][M][K], per `layout`) with
+ *     w[b][m][k] = exp(+2 pi i freqs[b] positions[k] sin(angles[m]) / c)
+ * (reading R9: raw sum, no 1/K).  positions: K receiver offsets d_k along the array (m);
+ * angles: M beam directions theta_m (rad); freqs: B channel frequencies (Hz); c > 0 wave speed
+ * (m/s).  All arrays are fp64 DEVICE pointers; the phase is reduced in fp64 before sincospi.
+ * Follow with tcbf_pack(plan, TCBF_WEIGHTS, ...). */
+tcbf_status tcbf_steering_weights(const tcbf_plan* plan, const double* positions, const double* angles,
+                                  const double* freqs, double c, tcbf_src_layout layout, float* dst,
+                                  void* stream);
+
 /* End-to-end convenience over HOST buffers (the e2e boundary): copies the fp32
  * data X (host, pinned recommended) to the device in batch chunks, packs it,
  * beamforms against the already packed device weights and copies the output back

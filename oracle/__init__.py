@@ -59,6 +59,8 @@ def lib():
             f = getattr(L, name)
             f.restype = ctypes.c_int
             f.argtypes = [vp, ctypes.c_int, ctypes.c_int, i64, i64, i64, i64, vp]
+        L.oracle_steering_weights.restype = ctypes.c_int
+        L.oracle_steering_weights.argtypes = [vp, vp, vp, ctypes.c_double, i64, i64, i64, vp]
         L.oracle_useful_ops.restype = ctypes.c_double
         L.oracle_useful_ops.argtypes = [i64, i64, i64, i64]
         _LIB = L
@@ -148,6 +150,19 @@ def pack_b1(src: np.ndarray, layout: int, operand: int, B: int, R: int, C: int,
     if rc != 0:
         raise ValueError(f"oracle_pack_b1 rc={rc}")
     return out
+
+
+def steering_weights(positions, angles, freqs, c: float) -> np.ndarray:
+    """complex128 [B][M][K]: exp(+2 pi i f_b d_k sin(theta_m) / c)."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64)
+    th = np.ascontiguousarray(angles, dtype=np.float64)
+    fr = np.ascontiguousarray(freqs, dtype=np.float64)
+    B, M, K = fr.size, th.size, pos.size
+    out = np.empty((B, M, K, 2), dtype=np.float64)
+    rc = lib().oracle_steering_weights(_ptr(pos), _ptr(th), _ptr(fr), float(c), B, M, K, _ptr(out))
+    if rc != 0:
+        raise ValueError(f"oracle_steering_weights rc={rc}")
+    return out[..., 0] + 1j * out[..., 1]
 
 
 def useful_ops(M: int, N: int, K: int, B: int) -> float:

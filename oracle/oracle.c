@@ -315,6 +315,24 @@ int oracle_pack_b1(const float* src, int layout, int operand, int64_t B, int64_t
   return OR_OK;
 }
 
+/* Steering weights (Eqs. 1-3): delay tau_k = d_k sin(theta) / c (Eq. 2);
+ * narrowband phase alignment w = exp(+2 pi i f tau_k) (reading R9).  Plain double
+ * cos/sin of the full phase; out is [B][M][K][2] (re, im). */
+int oracle_steering_weights(const double* pos, const double* theta, const double* freq, double c, int64_t B,
+                            int64_t M, int64_t K, double* out) {
+  if (!pos || !theta || !freq || !out || !(c > 0.0) || B < 1 || M < 1 || K < 1) return OR_EINVAL;
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int64_t b = 0; b < B; ++b)
+    for (int64_t m = 0; m < M; ++m)
+      for (int64_t k = 0; k < K; ++k) {
+        double tau = pos[k] * sin(theta[m]) / c;
+        double ph = two_pi * freq[b] * tau;
+        out[((b * M + m) * K + k) * 2 + 0] = cos(ph);
+        out[((b * M + m) * K + k) * 2 + 1] = sin(ph);
+      }
+  return OR_OK;
+}
+
 /* Useful operations: 8*M*N*K per complex GEMM. */
 double oracle_useful_ops(int64_t M, int64_t N, int64_t K, int64_t B) {
   return 8.0 * (double)M * (double)N * (double)K * (double)B;

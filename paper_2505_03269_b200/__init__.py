@@ -63,6 +63,8 @@ def lib():
         L.tcbf_beamform.argtypes = [vp, vp, vp, vp, vp]
         L.tcbf_beamform_raw.restype = ctypes.c_int
         L.tcbf_beamform_raw.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
+        L.tcbf_steering_weights.restype = ctypes.c_int
+        L.tcbf_steering_weights.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_int, vp, vp]
         L.tcbf_beamform_host.restype = ctypes.c_int
         L.tcbf_beamform_host.argtypes = [vp, vp, vp, ctypes.c_int, vp]
         L.tcbf_last_launch_count.restype = ctypes.c_int
@@ -175,6 +177,19 @@ class Plan:
     def raw_fused(self) -> bool:
         """True when beamform_raw runs the fused single-kernel path for this plan."""
         return self.precision == F16 and self.k_packed <= 256 and self.N % 4 == 0
+
+    def steering_weights(self, positions, angles, freqs, c, layout="interleaved", out=None, stream=None):
+        """fp32 weight source w[b][m][k] = exp(+2 pi i f_b d_k sin(theta_m) / c).
+        positions [K], angles [M], freqs [B]: cuda float64 tensors."""
+        import torch
+        if out is None:
+            shape = (self.batch, self.M, self.K, 2) if _LAYOUT[layout] == INTERLEAVED else (self.batch, 2, self.M, self.K)
+            out = torch.empty(shape, dtype=torch.float32, device=positions.device)
+        _check(lib().tcbf_steering_weights(self._h, ctypes.c_void_p(positions.data_ptr()),
+                                           ctypes.c_void_p(angles.data_ptr()), ctypes.c_void_p(freqs.data_ptr()),
+                                           float(c), _LAYOUT[layout], ctypes.c_void_p(out.data_ptr()),
+                                           _stream_ptr(stream, positions.device)), "tcbf_steering_weights")
+        return out
 
     def beamform_host(self, w_packed_dev, x_host, out_host, layout="interleaved"):
         """End-to-end over host buffers (torch CPU tensors, pinned for overlap)."""

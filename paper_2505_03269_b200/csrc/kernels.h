@@ -54,6 +54,10 @@ cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
                               cudaStream_t stream);
 
+// steering weights (steer.cu)
+cudaError_t launch_steering(const double* pos, const double* theta, const double* freq, double c, int64_t B,
+                            int64_t M, int64_t K, int layout, float* dst, cudaStream_t stream);
+
 // pack kernels (pack.cu)
 cudaError_t launch_pack_f16(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
                             int64_t K16, uint16_t* dst, cudaStream_t stream);

@@ -371,6 +371,25 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   return s;
 }
 
+tcbf_status tcbf_steering_weights(const tcbf_plan* plan, const double* positions, const double* angles,
+                                  const double* freqs, double c, tcbf_src_layout layout, float* dst,
+                                  void* stream) {
+  g_launches = 0;
+  if (!plan || !positions || !angles || !freqs || !dst) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (!(c > 0.0)) return fail(TCBF_ERR_INVALID_ARG, "wave speed must be > 0");
+  if (layout != TCBF_SRC_INTERLEAVED && layout != TCBF_SRC_PLANAR) return fail(TCBF_ERR_INVALID_ARG, "bad layout");
+  if (!aligned(dst, layout == TCBF_SRC_INTERLEAVED ? 8 : 4) || !aligned(positions, 8) || !aligned(angles, 8) ||
+      !aligned(freqs, 8))
+    return fail(TCBF_ERR_INVALID_ARG, "misaligned pointer");
+  tcbf_status s = check_device(plan);
+  if (s != TCBF_OK) return s;
+  cudaError_t e = tcbf::launch_steering(positions, angles, freqs, c, plan->B, plan->M, plan->K, (int)layout, dst,
+                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "steering kernel launch");
+  g_launches = 1;
+  return TCBF_OK;
+}
+
 int tcbf_last_launch_count(void) { return g_launches; }
 
 const char* tcbf_status_string(tcbf_status status) {

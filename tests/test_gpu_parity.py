@@ -262,6 +262,46 @@ def test_full_size_radio_f16_raw_sampled(tcbf):
         _check_f16(y[b][:, rows].cpu().numpy()[None], ref, w, x)
 
 
+# ------------------------------------------------------------------ steering weights (NEXT-3, Eq. 1-3)
+@pytest.mark.parametrize("layout", ["interleaved", "planar"])
+def test_steering_weights_vs_oracle(tcbf, layout):
+    rng = np.random.default_rng(8)
+    B, M, K = 3, 37, 48
+    c = 3e8
+    freqs = 110e6 + 1e6 * np.arange(B)                  # LOFAR HBA-like channels
+    pos = np.sort(rng.uniform(0, 3000.0, K))            # km-scale baselines: ~1e3 cycles of phase
+    th = np.deg2rad(np.linspace(-60, 60, M))
+    plan = tcbf.Plan(M, 64, K, B, "f16")
+    w = plan.steering_weights(torch.from_numpy(pos).cuda(), torch.from_numpy(th).cuda(),
+                              torch.from_numpy(freqs).cuda(), c, layout).cpu().numpy()
+    ref = oracle.steering_weights(pos, th, freqs, c)
+    got = w[..., 0] + 1j * w[..., 1] if layout == "interleaved" else w[:, 0] + 1j * w[:, 1]
+    # fp32 output of an fp64 phase; the oracle's cos/sin of a ~1e4 rad argument is itself only
+    # good to ~1e-12, so 2e-7 bounds the fp32 rounding of unit-modulus values
+    assert np.max(np.abs(got - ref)) < 2e-7
+
+
+def test_steered_beamform_coherent_gain(tcbf):
+    """Steering kernel -> pack -> beamform of a simulated plane wave: argmax at the source and
+    |y| = K within fp16 rounding (coherent gain)."""
+    c, f = 3e8, 150e6
+    K, M, N = 96, 121, 64
+    rng = np.random.default_rng(4)
+    pos = np.sort(rng.uniform(0, 40 * c / f, K))
+    th = np.deg2rad(np.linspace(-60, 60, M))
+    m0 = 77
+    s = np.exp(2j * np.pi * rng.uniform(size=N))
+    x = (np.exp(-2j * np.pi * f * pos * np.sin(th[m0]) / c)[:, None] * s[None, :]).astype(np.complex64)[None]
+    plan = tcbf.Plan(M, N, K, 1, "f16")
+    wsrc = plan.steering_weights(torch.from_numpy(pos).cuda(), torch.from_numpy(th).cuda(),
+                                 torch.tensor([f], dtype=torch.float64).cuda(), c)
+    y = plan.beamform_raw(plan.pack(tcbf.WEIGHTS, wsrc), _dev(synth.to_interleaved(x)))
+    torch.cuda.synchronize()
+    yc = y[0, 0].cpu().numpy() + 1j * y[0, 1].cpu().numpy()
+    assert np.all(np.argmax(np.abs(yc), axis=0) == m0)
+    assert np.allclose(np.abs(yc[m0]), K, rtol=2e-3)
+
+
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
 @pytest.fixture(params=["tc", "popc"])
 def b1_kernel(request, monkeypatch):
