@@ -6,7 +6,9 @@ import paper_2505_03269_b200 as tcbf
 import synth
 
 SHAPES = {"radio": (1024, 1024, 256, 256, "phase", "adc"), "sq8192": (8192, 8192, 8192, 1, "uniform", "uniform"),
-          "ultra": (65536, 256, 8192, 8, "phase_amp", "adc_scaled"), "sq4096": (4096, 4096, 4096, 1, "uniform", "uniform")}
+          "ultra": (65536, 256, 8192, 8, "phase_amp", "adc_scaled"), "sq4096": (4096, 4096, 4096, 1, "uniform", "uniform"),
+          "k512": (1024, 1024, 512, 256, "phase", "adc"), "k384": (1024, 1024, 384, 256, "phase", "adc"),
+          "k1024": (1024, 1024, 1024, 64, "phase", "adc"), "sq2048": (2048, 2048, 2048, 1, "uniform", "uniform")}
 variants = [int(v) for v in os.environ.get("VARIANTS", "0,1,2,3").split(",")]
 for name in sys.argv[1:] or ["radio", "sq8192"]:
     M, N, K, B, wd, xd = SHAPES[name]
