@@ -181,9 +181,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp < 2 + EPI_WARPS) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
-    const int ew = warp - 2;
     constexpr int CHUNKS = BN / 32;
-    uint8_t* stg = epi_base + ew * 8192;
     int sbuf = 0;
     int it = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -210,27 +208,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) mbar_arrive(&tempty[abuf]);
           }
           const uint32_t* vv = v[ch & 1];
-          if (lane == 0) bulk_wait_group_read<1>();
-          __syncwarp();
-          uint8_t* buf = stg + sbuf * 4096;
+          // cooperative staging: the 4 epilogue warps fill one 128-row x 32-column box (16 KB),
+          // one thread issues a single TMA store per chunk
+          uint8_t* buf = epi_base + sbuf * 16384;
+          if (threadIdx.x == 64) bulk_wait_group_read<1>();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const int row = q * 32 + lane;
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int pos = j ^ (lane & 7);
-            *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
+            const int pos = j ^ (row & 7);
+            *reinterpret_cast<uint4*>(buf + row * 128 + pos * 16) =
                 make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
           }
           fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64) {
+            tma_store_3d(&tmC, buf, n0 + c * 32, m0, 2 * b + part);
             bulk_commit_group();
           }
           sbuf ^= 1;
         }
       }
     }
-    if (lane == 0) bulk_wait_group<0>();
-    __syncwarp();
+    if (threadIdx.x == 64) bulk_wait_group<0>();
   } else {
     // ------------------------------------------------------------ converters: fp32 data -> resident B
     const int ct = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..255

@@ -41,7 +41,9 @@ struct F16Cfg {
   // registers (no smem traffic; needs N % 8 == 0), 2 = masked scalar stores (any N),
   // 3 = swizzled smem staging + coalesced 128-bit st.global (4 full lines per warp store,
   //     keeps the per-SM TMA engine free for the operand loads; needs N % 4 == 0)
-  static constexpr int EPI_BYTES = (EPI == 0 || EPI == 3) ? EPI_WARPS * EPI_BUFS * 4096 : 0;
+  //     4 = cooperative staging: the 4 epilogue warps fill one 128-row x 32-column box (16 KB)
+  //         and one thread issues a single TMA store per chunk (4x fewer bulk operations)
+  static constexpr int EPI_BYTES = (EPI == 0 || EPI == 3 || EPI == 4) ? EPI_WARPS * EPI_BUFS * 4096 : 0;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x (D_r, D_i)
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
@@ -226,7 +228,27 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
         }
         const uint32_t* vv = v[i & 1];
         if (args.debug & 1) continue;
-        if constexpr (EPI == 0) {
+        if constexpr (EPI == 4) {
+          static_assert(EPI_WARPS == 4, "cooperative epilogue uses exactly 4 warps");
+          // buffer sbuf: 128 rows x 128 B; warp q owns rows 32q..32q+31 (the TMEM quadrant)
+          uint8_t* buf = epi_base + sbuf * 16384;
+          if (threadIdx.x == 64) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();  // issuing thread (warp 2)
+          asm volatile("bar.sync 1, 128;" ::: "memory");                  // buffer free for everyone
+          const int row = q * 32 + lane;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pos = j ^ (row & 7);
+            *reinterpret_cast<uint4*>(buf + row * 128 + pos * 16) =
+                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+          }
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 128;" ::: "memory");                  // box complete
+          if (threadIdx.x == 64) {
+            tma_store_3d(&tmC, buf, n0 + c * 32, m0, 2 * b + part);
+            bulk_commit_group();
+          }
+          sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
+        } else if constexpr (EPI == 0) {
           if (lane == 0) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();
           __syncwarp();
           uint8_t* buf = stg + sbuf * 4096;
@@ -293,6 +315,9 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
         }
       }
     }
+    if constexpr (EPI == 4) {
+      if (threadIdx.x == 64) bulk_wait_group<0>();
+    }
     if constexpr (EPI == 0) {
       if (lane == 0) bulk_wait_group<0>();
       __syncwarp();
@@ -335,6 +360,7 @@ cudaError_t dispatch(int variant, int epi, const CUtensorMap& a, const CUtensorM
     case F16_V_K64_S3_DIRECT_E8: return launch_impl<128, 64, 3, 8, 1>(a, b, c, g, sms, s);
     case F16_V_K64_S3_STG: return launch_impl<128, 64, 3, 4, 3>(a, b, c, g, sms, s);
     case F16_V_K64_S3_STG_E8: return launch_impl<128, 64, 2, 8, 3>(a, b, c, g, sms, s);
+    case F16_V_K64_S3_COOP: return launch_impl<128, 64, 3, 4, 4>(a, b, c, g, sms, s);
     default:              return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
   }
 }

@@ -28,7 +28,8 @@ enum {
   F16_V_2CTA_N256 = 8,  // CTA pair, 256x256 tile, BK 64, 3 stages, single TMEM buffer
   F16_V_K64_S3_STG = 9,     // 128x128, BK 64, 3 stages, smem-staged coalesced st.global epilogue
   F16_V_K64_S3_STG_E8 = 10, // same, 2 stages, 8 epilogue warps
-  F16_V_COUNT = 11
+  F16_V_K64_S3_COOP = 11,   // 128x128, BK 64, 3 stages, cooperative 128-row TMA-store boxes
+  F16_V_COUNT = 12
 };
 int gemm_f16_block_n(int variant);
 cudaError_t launch_gemm_f16_2cta(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,

@@ -160,7 +160,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   else if (M <= 128 || N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
   else if (K >= 2048 && N >= 256) p->f16_variant = tcbf::F16_V_2CTA_N256;   // long K: compute-bound
   else if (kp > 256) p->f16_variant = tcbf::F16_V_2CTA_N128;              // mid K (measured +5-8%)
-  else p->f16_variant = tcbf::F16_V_K64_S3;                               // short K: store-bound
+  else p->f16_variant = tcbf::F16_V_K64_S3_COOP;                          // short K: store-bound
   if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
@@ -199,7 +199,7 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
       "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
       "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma", "f16_tcgen05_128x128_k64s3e4_stg256",
       "f16_tcgen05_128x128_k64s3e8_stg256", "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma",
-      "f16_tcgen05_128x128_k64s3e4_stgco", "f16_tcgen05_128x128_k64s2e8_stgco"};
+      "f16_tcgen05_128x128_k64s3e4_stgco", "f16_tcgen05_128x128_k64s2e8_stgco", "f16_tcgen05_128x128_k64s3e4_coop"};
   if (plan->N % 8 != 0 && plan->N % 4 != 0) return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked"
                                                                                       : "f16_tcgen05_128x128_masked";
   return names[plan->f16_variant];
@@ -246,7 +246,8 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     int var = plan->f16_variant;
     const bool direct = var == tcbf::F16_V_K64_S3_DIRECT || var == tcbf::F16_V_K64_S3_DIRECT_E8;
     const bool stgco = var == tcbf::F16_V_K64_S3_STG || var == tcbf::F16_V_K64_S3_STG_E8;
-    int epi = direct ? 1 : (stgco ? 3 : 0);
+    const bool coop = var == tcbf::F16_V_K64_S3_COOP;
+    int epi = direct ? 1 : (stgco ? 3 : (coop ? 4 : 0));
     if (plan->N % 4 != 0) {
       epi = 2;
       if (var != tcbf::F16_V_N64) var = tcbf::F16_V_K64_S3;
@@ -267,9 +268,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->n_packed, plan->K, 2 * plan->B, 64, bk,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
-    if (tma_store) {
-      s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (tma_store || epi == 4) {
+      s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32,
+                    epi == 4 ? 128 : 32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
       if (s != TCBF_OK) return s;
     } else {
       memset(&tc, 0, sizeof(tc));
@@ -345,7 +346,7 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
-    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 128,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
     if (s != TCBF_OK) return s;
     tcbf::GemmF16Args a;

@@ -125,7 +125,7 @@ F16_SHAPES = [
 ]
 
 
-@pytest.fixture(params=["default", "0", "5", "1", "7", "8", "9", "10"])
+@pytest.fixture(params=["default", "0", "5", "1", "7", "8", "9", "10", "11"])
 def f16_variant(request, monkeypatch):
     """fp16 kernel variants: default table choice, BK32/8-warp TMA-store, direct 256-bit stores."""
     if request.param != "default":
