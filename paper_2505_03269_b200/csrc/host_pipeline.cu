@@ -3,7 +3,7 @@
 // host->device copy of chunk i+1 and the device->host copy of chunk i-1 overlap the
 // pack + beamform kernels of chunk i (copy engines and SMs work concurrently).
 // Weights are packed once and stay resident (the model matrix is packed
-// once, the measurement matrix per ensemble).
+// once, the measurement matrix per ensemble).  Each chunk runs tcbf_beamform_raw.
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -20,7 +20,7 @@ extern "C" tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_p
   const size_t wp_per_b = plan->w_bytes / B;
   const size_t out_per_b = plan->out_bytes / B;
   // chunk: ~192 MiB of device scratch per buffer set, at least one batch entry
-  const size_t per_b = src_per_b + xp_per_b + out_per_b;
+  const size_t per_b = src_per_b + out_per_b;  // packed data scratch (if any) is tcbf_beamform_raw's
   int64_t cb = (int64_t)((192ull << 20) / per_b);
   if (cb < 1) cb = 1;
   if (cb > B) cb = B;
@@ -39,8 +39,7 @@ extern "C" tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_p
     const int64_t b0 = c * cb;
     const int64_t nb = (b0 + cb <= B) ? cb : (B - b0);
     char* d_src = static_cast<char*>(buf[s]);
-    char* d_xp = d_src + src_per_b * cb;
-    char* d_out = d_xp + xp_per_b * cb;
+    char* d_out = d_src + src_per_b * cb;
     tcbf_plan sub = *plan;  // same shape, nb batch entries
     sub.B = nb;
     sub.w_bytes = wp_per_b * nb;
@@ -48,10 +47,9 @@ extern "C" tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_p
     sub.out_bytes = out_per_b * nb;
     if (cudaMemcpyAsync(d_src, reinterpret_cast<const char*>(x_host) + src_per_b * b0, src_per_b * nb,
                         cudaMemcpyHostToDevice, st[s]) != cudaSuccess) { status = TCBF_ERR_CUDA; break; }
-    status = tcbf_pack(&sub, TCBF_DATA, reinterpret_cast<const float*>(d_src), layout, d_xp, st[s]);
-    if (status != TCBF_OK) break;
-    launches += tcbf_last_launch_count();
-    status = tcbf_beamform(&sub, static_cast<const char*>(w_packed_dev) + wp_per_b * b0, d_xp, d_out, st[s]);
+    // pack + beamform (one fused kernel where the plan allows it)
+    status = tcbf_beamform_raw(&sub, static_cast<const char*>(w_packed_dev) + wp_per_b * b0,
+                               reinterpret_cast<const float*>(d_src), layout, d_out, st[s]);
     if (status != TCBF_OK) break;
     launches += tcbf_last_launch_count();
     if (cudaMemcpyAsync(static_cast<char*>(out_host) + out_per_b * b0, d_out, out_per_b * nb,

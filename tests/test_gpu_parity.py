@@ -302,6 +302,50 @@ def test_steered_beamform_coherent_gain(tcbf):
     assert np.allclose(np.abs(yc[m0]), K, rtol=2e-3)
 
 
+# ------------------------------------------------------------------ end-to-end host pipeline and ABI errors
+@pytest.mark.parametrize("prec", ["f16", "b1"])
+def test_beamform_host_equals_device_path(tcbf, prec):
+    """tcbf_beamform_host (chunked H2D -> pack -> beamform -> D2H on two streams) returns exactly
+    the device path's output, for a batch that spans several chunks."""
+    M, N, K, B = 256, 512, 128, 24
+    w = synth.to_interleaved(synth.generate("phase", 6, 0, B, M, K))
+    x = synth.to_interleaved(synth.generate("adc", 6, 1, B, K, N))
+    plan = tcbf.Plan(M, N, K, B, prec)
+    wp = plan.pack(tcbf.WEIGHTS, _dev(w))
+    ref = plan.beamform(wp, plan.pack(tcbf.DATA, _dev(x)))
+    x_host = torch.from_numpy(x).pin_memory()
+    out_host = torch.empty(tuple(ref.shape), dtype=ref.dtype).pin_memory()
+    plan.beamform_host(wp, x_host, out_host)
+    torch.cuda.synchronize()
+    assert torch.equal(out_host, ref.cpu())
+
+
+def test_abi_errors_on_device(tcbf):
+    import ctypes
+    L = tcbf.lib()
+    plan = tcbf.Plan(64, 64, 64, 1, "f16")
+    wp = plan.alloc_packed(tcbf.WEIGHTS)
+    xp = plan.alloc_packed(tcbf.DATA)
+    out = plan.alloc_output()
+    vp = ctypes.c_void_p
+    # misaligned output / packed pointers -> INVALID_ARG, nothing launched
+    assert L.tcbf_beamform(plan._h, vp(wp.data_ptr()), vp(xp.data_ptr()), vp(out.data_ptr() + 4), None) == 1
+    assert L.tcbf_beamform(plan._h, vp(wp.data_ptr() + 8), vp(xp.data_ptr()), vp(out.data_ptr()), None) == 1
+    assert L.tcbf_last_launch_count() == 0
+    src = torch.zeros((1, 64, 64, 2), device="cuda")
+    assert L.tcbf_pack(plan._h, 0, vp(src.data_ptr() + 4), 0, vp(wp.data_ptr()), None) == 1   # 8-B rule
+    assert L.tcbf_pack(plan._h, 7, vp(src.data_ptr()), 0, vp(wp.data_ptr()), None) == 1       # bad operand
+    assert L.tcbf_pack(plan._h, 0, vp(src.data_ptr()), 5, vp(wp.data_ptr()), None) == 1       # bad layout
+    assert b"aligned" in L.tcbf_last_error() or b"layout" in L.tcbf_last_error()
+    d = torch.zeros(4, dtype=torch.float64, device="cuda")
+    assert L.tcbf_steering_weights(plan._h, vp(d.data_ptr()), vp(d.data_ptr()), vp(d.data_ptr()),
+                                   ctypes.c_double(-1.0), 0, vp(src.data_ptr()), None) == 1    # c <= 0
+    # a valid call still works afterwards and reports one launch
+    assert L.tcbf_beamform(plan._h, vp(wp.data_ptr()), vp(xp.data_ptr()), vp(out.data_ptr()), None) == 0
+    assert L.tcbf_last_launch_count() == 1
+    torch.cuda.synchronize()
+
+
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
 @pytest.fixture(params=["tc", "popc"])
 def b1_kernel(request, monkeypatch):
