@@ -165,8 +165,12 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
   }
-  p->b1_tc = 1;
-  if (const char* env = getenv("TCBF_B1_KERNEL")) p->b1_tc = strcmp(env, "popc") == 0 ? 0 : 1;
+  p->b1_tc = tcbf::gemm_b1_f8_supported(kp) ? 2 : 1;
+  if (const char* env = getenv("TCBF_B1_KERNEL")) {
+    if (strcmp(env, "popc") == 0) p->b1_tc = 0;
+    else if (strcmp(env, "i8") == 0) p->b1_tc = 1;
+    else if (strcmp(env, "f8") == 0 && tcbf::gemm_b1_f8_supported(kp)) p->b1_tc = 2;
+  }
   *plan = p;
   return TCBF_OK;
 }
@@ -193,6 +197,7 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (!plan) return "none";
   if (plan->prec == TCBF_PREC_B1) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
+    if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
   static const char* names[tcbf::F16_V_COUNT] = {
@@ -314,12 +319,13 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;
       memset(&tc, 0, sizeof(tc));
-      if (tma_store) {
-        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+      if (tma_store) {  // f8 kernel stores cooperative 128-row boxes, i8 kernel per-warp 32-row boxes
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32,
+                      plan->b1_tc == 2 ? 128 : 32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (s != TCBF_OK) return s;
       }
-      e = tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
+      e = plan->b1_tc == 2 ? tcbf::launch_gemm_b1_f8(tc, a, tma_store, plan->num_sms, st)
+                           : tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
     } else {
       e = tcbf::launch_gemm_b1_popc(a, st);
     }

@@ -347,9 +347,10 @@ def test_abi_errors_on_device(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
-@pytest.fixture(params=["tc", "popc"])
+@pytest.fixture(params=["f8", "i8", "popc"])
 def b1_kernel(request, monkeypatch):
-    """Both 1-bit kernels: tcgen05 kind::i8 (default) and the CUDA-core XOR/popc kernel."""
+    """All 1-bit kernels: tcgen05 kind::f8f6f4 on +-1 (default), tcgen05 kind::i8 AND form,
+    and the CUDA-core XOR/popc kernel."""
     monkeypatch.setenv("TCBF_B1_KERNEL", request.param)
     return request.param
 
@@ -394,6 +395,21 @@ def test_b1_random_corpus(tcbf, b1_kernel):
         x = rng.standard_normal((1, K, N, 2)).astype(np.float32)
         _, _, _, y = _run(tcbf, "b1", w, x, M, N, K, 1)
         assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, M, N, K, 1)), (M, N, K)
+
+
+def test_b1_large_k_exact(tcbf, b1_kernel):
+    """Long K: partial sums up to ~2^17 (f8: exact fp32 accumulation of +-1 products)."""
+    M, N, K, B = 16, 24, 65536 + 7, 1
+    rng = np.random.default_rng(21)
+    w = rng.standard_normal((B, M, K, 2)).astype(np.float32)
+    x = rng.standard_normal((B, K, N, 2)).astype(np.float32)
+    # make a few outputs near the extremes: a matched beam (y = 2K) and its negative
+    x[0, :, 0, :] = w[0, 3, :, :] * np.array([1, -1], np.float32)
+    x[0, :, 1, :] = -x[0, :, 0, :]
+    _, _, _, y = _run(tcbf, "b1", w, x, M, N, K, B)
+    ref = oracle.cgemm_b1(w, x, 0, M, N, K, B)
+    assert ref[0, 0, 3, 0] == 2 * K and ref[0, 0, 3, 1] == -2 * K
+    assert np.array_equal(y, ref)
 
 
 # ------------------------------------------------------------------ full-size sampled parity
