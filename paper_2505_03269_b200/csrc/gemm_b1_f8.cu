@@ -16,7 +16,7 @@
 //
 // Roles (persistent CTA per SM, 416 threads):
 //   warp 0      TMEM allocator + single-thread MMA issuer (4 MMAs per K=32 step)
-//   warps 1-4   epilogue: tcgen05.ld, fp32 -> int32, Im - 2 K_pad, TMA store of int32 (128-row boxes)
+//   warps 1-4   epilogue: tcgen05.ld, fp32 -> int32, Im - 2 K_pad, TMA store of int32
 //   warps 5-8   expanders for A_r, A_i (one weight row per thread)
 //   warps 9-12  expanders for B_r, B_i (one data column per thread)
 #include <cstdint>
@@ -35,7 +35,7 @@ constexpr int KB_WORDS = 4;            // 128 bits per K block -> 128 expanded b
 constexpr int TILE_BYTES = 128 * 128;  // one expanded operand tile (rows x 128 B)
 constexpr int STAGES = 3;
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;  // A_r, A_i, B_r, B_i
-constexpr int EPI_BYTES = 2 * 16384;         // two 128-row x 32-column int32 boxes
+constexpr int EPI_BYTES = 4 * 2 * 4096;      // per epilogue warp: two 32-row x 32-column int32 boxes
 constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
 constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
 constexpr int NUM_THREADS = 13 * 32;
@@ -155,7 +155,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr int CHUNKS = BN / 32;
     int sbuf = 0;
     int it = 0;
-    const int issuer = 32;  // threadIdx.x of warp 1 lane 0 issues the cooperative TMA stores
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       int b, mt, nt;
       tile_coords(t, tiles_m, tiles_n, p.group_m, b, mt, nt);
@@ -184,21 +183,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = (uint32_t)(__float2int_rn(__uint_as_float(v[j])) - corr);
         if (p.debug & 1) continue;
-        if constexpr (TMA_STORE) {
-          uint8_t* buf = epi_base + sbuf * 16384;
-          if (threadIdx.x == issuer) bulk_wait_group_read<1>();
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          const int row = q * 32 + lane;
+        if constexpr (TMA_STORE) {  // per-warp 32-row boxes, 2 staging buffers per warp
+          uint8_t* buf = epi_base + ((warp - 1) * 2 + sbuf) * 4096;
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const int pos = j ^ (row & 7);
-            *reinterpret_cast<uint4*>(buf + row * 128 + pos * 16) =
+            const int pos = j ^ (lane & 7);
+            *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
           fence_proxy_async_smem();
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (threadIdx.x == issuer) {
-            tma_store_3d(&tmC, buf, n0 + c * 32, m0, 2 * b + part);
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
             bulk_commit_group();
           }
           sbuf ^= 1;
@@ -216,7 +214,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
     if constexpr (TMA_STORE) {
-      if (threadIdx.x == issuer) bulk_wait_group<0>();
+      if (lane == 0) bulk_wait_group<0>();
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ expanders

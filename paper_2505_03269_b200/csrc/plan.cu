@@ -165,7 +165,8 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
   }
-  p->b1_tc = tcbf::gemm_b1_f8_supported(kp) ? 2 : 1;
+  // int8 AND-form kernel by default (measured faster than the +-1 fp8 kernel on radio and square)
+  p->b1_tc = 1;
   if (const char* env = getenv("TCBF_B1_KERNEL")) {
     if (strcmp(env, "popc") == 0) p->b1_tc = 0;
     else if (strcmp(env, "i8") == 0) p->b1_tc = 1;
@@ -319,9 +320,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;
       memset(&tc, 0, sizeof(tc));
-      if (tma_store) {  // f8 kernel stores cooperative 128-row boxes, i8 kernel per-warp 32-row boxes
-        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32,
-                      plan->b1_tc == 2 ? 128 : 32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+      if (tma_store) {  // per-warp 32-row x 32-column boxes
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (s != TCBF_OK) return s;
       }
       e = plan->b1_tc == 2 ? tcbf::launch_gemm_b1_f8(tc, a, tma_store, plan->num_sms, st)
