@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int num_kb = p.Kw / KB_WORDS;
+  const int num_items = num_tiles * p.splits;  // (tile, K split) work items
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -137,13 +138,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++it) {
+        const int sp = item % p.splits;
+        const int kb0 = sp * p.kb_per_split, kb1 = min(num_kb, kb0 + p.kb_per_split);
         const int abuf = it & 1;
         mbar_wait(&tempty_bar[abuf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_re = tmem_base + abuf * 2 * BN;
         const uint32_t d_im = d_re + BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           uint8_t* st = smem + stage * STAGE_BYTES;
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
             const uint64_t br = smem_desc_k128(sBr, off), bi = smem_desc_k128(sBi, off);
             const uint64_t bc = smem_desc_k128(sBc, off);
-            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            const uint32_t acc = ((kb - kb0) | kk) ? 1u : 0u;
             if (p.debug & 2) continue;
             mma_i8_ss(d_re, ar, br, IDESC, acc);  // P(A_r & B_r)
             mma_i8_ss(d_re, ai, bc, IDESC, 1u);   // P(A_i & ~B_i)
@@ -179,7 +182,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint8_t* stg = epi_base + ew * 8192;
     int sbuf = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++it) {
+      const int t = item / p.splits;
       int b, mt, nt;
       tile_coords(t, tiles_m, tiles_n, p.group_m, b, mt, nt);
       const int m0 = mt * BM;
@@ -238,7 +242,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
+            if (p.splits > 1) tma_reduce_add_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
+            else tma_store_3d(&tmC, buf, n0 + c * 32, m0 + q * 32, 2 * b + part);
             bulk_commit_group();
           }
           sbuf ^= 1;
@@ -248,7 +253,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = n0 + c * 32 + j;
-              if (n < p.N) row[n] = (int32_t)v[j];
+              if (n < p.N) {
+                if (p.splits > 1) atomicAdd(row + n, (int32_t)v[j]);
+                else row[n] = (int32_t)v[j];
+              }
             }
           }
         }
@@ -288,24 +296,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     const uint4* src_r;
     const uint4* src_i;
-    row_ptrs(blockIdx.x, src_r, src_i);
-    uint4 nr = (blockIdx.x < (unsigned)num_tiles && src_r) ? __ldg(src_r) : zero;
-    uint4 ni = (blockIdx.x < (unsigned)num_tiles && src_i) ? __ldg(src_i) : zero;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      int pc_r = 0, pc_i = 0;  // popcounts of this row / column (real, imaginary plane)
+    auto item_range = [&](int item, int& kb0, int& kb1) {
+      const int sp = item % p.splits;
+      kb0 = sp * p.kb_per_split;
+      kb1 = min(num_kb, kb0 + p.kb_per_split);
+    };
+    row_ptrs(blockIdx.x / p.splits, src_r, src_i);
+    int kb0, kb1;
+    item_range(blockIdx.x, kb0, kb1);
+    uint4 nr = (blockIdx.x < (unsigned)num_items && src_r) ? __ldg(src_r + kb0) : zero;
+    uint4 ni = (blockIdx.x < (unsigned)num_items && src_i) ? __ldg(src_i + kb0) : zero;
+    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++it) {
+      int pc_r = 0, pc_i = 0;  // popcounts of this row / column over the item's K range
       const bool valid = src_r != nullptr;
       const uint4* next_r = nullptr;
       const uint4* next_i = nullptr;
-      const int tn = t + gridDim.x;
-      if (tn < num_tiles) row_ptrs(tn, next_r, next_i);
-      for (int kb = 0; kb < num_kb; ++kb) {
+      const int in = item + gridDim.x;
+      int nkb0 = 0, nkb1 = 0;
+      if (in < num_items) {
+        row_ptrs(in / p.splits, next_r, next_i);
+        item_range(in, nkb0, nkb1);
+      }
+      for (int kb = kb0; kb < kb1; ++kb) {
         const uint4 wr = nr, wi = ni;
-        if (kb + 1 < num_kb) {
+        if (kb + 1 < kb1) {
           nr = valid ? __ldg(src_r + kb + 1) : zero;
           ni = valid ? __ldg(src_i + kb + 1) : zero;
-        } else {  // first K block of this thread's next tile
-          nr = next_r ? __ldg(next_r) : zero;
-          ni = next_i ? __ldg(next_i) : zero;
+        } else {  // first K block of this thread's next work item
+          nr = next_r ? __ldg(next_r + nkb0) : zero;
+          ni = next_i ? __ldg(next_i + nkb0) : zero;
         }
         pc_r += __popc(wr.x) + __popc(wr.y) + __popc(wr.z) + __popc(wr.w);
         pc_i += __popc(wi.x) + __popc(wi.y) + __popc(wi.z) + __popc(wi.w);
@@ -340,12 +359,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         colsum[(cb * 3 + 0) * 128 + row] = -2 * (pc_r + pc_i);
       } else {
         colsum[(cb * 3 + 1) * 128 + row] = 2 * (pc_i - pc_r);
-        colsum[(cb * 3 + 2) * 128 + row] = 2 * p.K - 2 * (pc_r + pc_i);
+        // logical K positions of this item's range (padding bits are 0 and count nothing)
+        const int k_s = max(0, min(p.K, kb1 * 128) - kb0 * 128);
+        colsum[(cb * 3 + 2) * 128 + row] = 2 * k_s - 2 * (pc_r + pc_i);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sfull_bar[cb]);
       src_r = next_r;
       src_i = next_i;
+      kb0 = nkb0;
+      kb1 = nkb1;
     }
   }
 

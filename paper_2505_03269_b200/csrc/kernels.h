@@ -50,6 +50,8 @@ struct GemmB1Args {
   int M, N, K, Kw, B;
   int debug;  // ablation (TCBF_DEBUG): bit0 skip stores, bit1 skip MMAs, bit2 skip expansion
   int group_m;  // tile rows per rasterisation group (tile_coords)
+  int splits;   // split-K factor (int8 kernel): >1 accumulates exact int32 partials with TMA reduce-add
+  int kb_per_split;
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 bool gemm_b1_f8_supported(int64_t Kw);

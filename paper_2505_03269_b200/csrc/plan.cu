@@ -316,6 +316,27 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
       const int64_t tm = (plan->M + 127) / 128;
       a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bytes_per_tile_row, tm));
     }
+    a.splits = 1;
+    a.kb_per_split = (int)(plan->kp / 4);
+    if (plan->b1_tc == 1) {
+      // split-K (exact int32 partials combined with TMA reduce-add)
+      const int64_t tiles = ((plan->M + 127) / 128) * ((plan->N + 127) / 128) * plan->B;
+      const int64_t nkb = plan->kp / 4;
+      // Measured: splitting does not shorten the per-SM chain of K blocks (the same total K-block
+      // count is spread over the SMs), so it is off by default and only forced for tests.
+      (void)tiles;
+      if (const char* env = getenv("TCBF_B1_SPLITS")) {
+        int64_t sp = std::min<int64_t>(std::max(1, atoi(env)), nkb);
+        if (sp > 1) {
+          a.kb_per_split = (int)((nkb + sp - 1) / sp);
+          a.splits = (int)((nkb + a.kb_per_split - 1) / a.kb_per_split);
+        }
+      }
+    }
+    if (a.splits > 1) {
+      e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
+    }
     if (plan->b1_tc) {
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;
@@ -330,11 +351,15 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
     } else {
       e = tcbf::launch_gemm_b1_popc(a, st);
     }
+    if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
+    g_launches = a.splits > 1 ? 2 : 1;  // memset + kernel when split-K
+    return TCBF_OK;
   }
   if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
   g_launches = 1;
   return TCBF_OK;
 }
+
 
 tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
                               tcbf_src_layout layout, void* out, void* stream) {

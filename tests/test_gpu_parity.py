@@ -397,6 +397,20 @@ def test_b1_random_corpus(tcbf, b1_kernel):
         assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, M, N, K, 1)), (M, N, K)
 
 
+@pytest.mark.parametrize("splits", ["auto", "3", "7"])
+def test_b1_split_k_bit_exact(tcbf, monkeypatch, splits):
+    """Split-K (int8 kernel, TMA reduce-add of exact int32 partials): the M=32 sweep shape class
+    and a ragged-N shape (atomic masked path), forced split counts included."""
+    if splits != "auto":
+        monkeypatch.setenv("TCBF_B1_SPLITS", splits)
+    for (M, N, K, B) in [(32, 512, 4096 + 5, 1), (40, 77, 3000, 2)]:
+        w = synth.generate("adc", 14, 0, B, M, K)
+        x = synth.generate("adc", 14, 1, B, K, N)
+        _, _, _, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+        ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
+        assert np.array_equal(y, ref), (M, N, K, B, splits)
+
+
 def test_b1_large_k_exact(tcbf, b1_kernel):
     """Long K: partial sums up to ~2^17 (f8: exact fp32 accumulation of +-1 products)."""
     M, N, K, B = 16, 24, 65536 + 7, 1
