@@ -159,8 +159,16 @@ class ClockSampler:
                 pass
             time.sleep(0.01)
 
+    def energy_mj(self):
+        """Total energy counter in mJ (NVML; PAPER.md:278 measures TOPs/J the same way via PMT)."""
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h))
+        except Exception:
+            return None
+
     def start(self):
         if self.ok:
+            self.e0 = self.energy_mj()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
 
@@ -168,6 +176,12 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            self.e1 = self.energy_mj()
+
+    def joules(self):
+        if not self.ok or getattr(self, "e0", None) is None or getattr(self, "e1", None) is None:
+            return None
+        return (self.e1 - self.e0) / 1e3
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -405,6 +419,12 @@ def run_tcbf(args, c):
         "gpu_launches": (1 if fused else 2) * args.steps,
         "clocks": sampler.summary(),
     }
+    j = sampler.joules()
+    if j is not None and j > 0:   # whole-board energy over the timed region (NEXT-4, Table III TOPs/J)
+        j = max_over_ranks(j, dev) if world == 1 else j
+        line["energy"] = {"joules_per_step": round(j / args.steps, 6),
+                          "teraops_per_joule": round(useful_ops(c) / (j / args.steps) / 1e12, 3),
+                          "source": "NVML total energy counter, this GPU, timed region"}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c)
     if rank == 0:
