@@ -171,6 +171,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     if (strcmp(env, "popc") == 0) p->b1_tc = 0;
     else if (strcmp(env, "i8") == 0) p->b1_tc = 1;
     else if (strcmp(env, "f8") == 0 && tcbf::gemm_b1_f8_supported(kp)) p->b1_tc = 2;
+    else if (strcmp(env, "i8pair") == 0) p->b1_tc = 3;
   }
   *plan = p;
   return TCBF_OK;
@@ -199,6 +200,7 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (plan->prec == TCBF_PREC_B1) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
     if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
+    if (plan->b1_tc == 3) return plan->N % 4 ? "b1_tcgen05_i8_2cta_256x128_stg" : "b1_tcgen05_i8_2cta_256x128_tma";
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
   static const char* names[tcbf::F16_V_COUNT] = {
@@ -346,8 +348,13 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (s != TCBF_OK) return s;
       }
+      if (plan->b1_tc == 3) {  // CTA pair: 256-row pair tiles
+        const int64_t bpr = 256 * plan->kp * 8;
+        a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bpr, (plan->M + 255) / 256));
+      }
       e = plan->b1_tc == 2 ? tcbf::launch_gemm_b1_f8(tc, a, tma_store, plan->num_sms, st)
-                           : tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
+          : plan->b1_tc == 3 ? tcbf::launch_gemm_b1_2cta(tc, a, tma_store, plan->num_sms, st)
+                             : tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
     } else {
       e = tcbf::launch_gemm_b1_popc(a, st);
     }

@@ -347,7 +347,7 @@ def test_abi_errors_on_device(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
-@pytest.fixture(params=["f8", "i8", "popc"])
+@pytest.fixture(params=["f8", "i8", "i8pair", "popc"])
 def b1_kernel(request, monkeypatch):
     """All 1-bit kernels: tcgen05 kind::f8f6f4 on +-1 (default), tcgen05 kind::i8 AND form,
     and the CUDA-core XOR/popc kernel."""
