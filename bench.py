@@ -46,6 +46,10 @@ CONFIGS = {
                      "radio astronomy 1-bit: M=1024 beams, K=512 stations, N=4096 samples, batch=256 channels"),
     "ultrasound_f16": _cfg("f16", 65536, 256, 8192, 8, "phase_amp", "adc_scaled", 3,
                            "computational ultrasound fp16: M=65536 pixels, K=8192, N=256 frames, batch=8"),
+    # ultrasound 1-bit real-time pipeline (Fig. 5): three orthogonal 128^2 planes,
+    # K = 128 frequencies x 64 transceivers x 32 transmissions, a block of 1024 frames per step
+    "ultrasound_b1_planes": _cfg("b1", 3 * 128 * 128, 1024, 128 * 64 * 32, 1, "phase_amp", "adc_scaled", 3,
+                                 "ultrasound 1-bit: M=49152 voxels (3 planes), K=262144, N=1024 frames"),
     # Fig. 3 extra rows
     "fig3_f16_small": _cfg("f16", 1024, 1024, 64, 256, "uniform", "uniform", 4, "fp16 small 256x1024x1024x64"),
     "fig3_b1_small": _cfg("b1", 1024, 1024, 256, 256, "uniform", "uniform", 4, "int1 small 256x1024x1024x256"),
@@ -292,6 +296,35 @@ def run_reference(args, c):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def pack_weights(plan, c, seed, dev, b0, max_src_bytes=8 << 30):
+    """Generate + pack the weights once (outside the timed region).  Model matrices whose fp32
+    source would not fit comfortably (ultrasound 1-bit: 103 GB) are generated and packed in row
+    slices of the same global index space and copied into the plan's [B][2][M][Kp] layout."""
+    import torch
+
+    import paper_2505_03269_b200 as tcbf
+    import synth
+    B, M, K = c["B"], c["M"], c["K"]
+    if B * M * K * 8 <= max_src_bytes:
+        wsrc = synth.generate_device(c["wd"], seed, 0, B, M, K, device=dev, b0=b0)
+        return plan.pack(tcbf.WEIGHTS, wsrc)
+    assert B == 1, "row-sliced weight generation implemented for batch 1"
+    wp = plan.alloc_packed(tcbf.WEIGHTS, dev)
+    rows = max(1, max_src_bytes // (K * 8))
+    for m0 in range(0, M, rows):
+        mr = min(rows, M - m0)
+        sub = tcbf.Plan(mr, c["N"], K, 1, c["prec"])
+        # rows m0..m0+mr of entry b0 of the global [*, M, K] weight tensor: element offset (b0*M + m0)*K
+        src = synth.generate_device(c["wd"], seed, 0, 1, mr, K, device=dev, b0=0,
+                                    offset_elems=(b0 * M + m0) * K)
+        part = sub.pack(tcbf.WEIGHTS, src)
+        del src
+        wp[0, :, m0:m0 + mr].copy_(part[0])
+        del part
+    torch.cuda.synchronize()
+    return wp
+
+
 def run_tcbf(args, c):
     import torch
     import torch.distributed as dist
@@ -317,9 +350,7 @@ def run_tcbf(args, c):
     seed = synth.SEED_BASE + c["idx"]
     plan = tcbf.Plan(M, N, K, B, c["prec"])
 
-    wsrc = synth.generate_device(c["wd"], seed, 0, B, M, K, device=dev, b0=sh.b0)
-    wp = plan.pack(tcbf.WEIGHTS, wsrc)
-    del wsrc
+    wp = pack_weights(plan, c, seed, dev, sh.b0)
     xsrc = synth.generate_device(c["xd"], seed, 1, B, K, N, device=dev, b0=sh.b0)
     xp = plan.alloc_packed(tcbf.DATA, dev)
     out = plan.alloc_output(dev)
@@ -375,6 +406,7 @@ def run_tcbf(args, c):
     ms_step = max_over_ranks(total_ms / args.steps, dev)
     gemm_ms_max = max_over_ranks(gemm_ms, dev)
     value = world * useful_ops(c) / (ms_step * 1e-3) / 1e12
+    frames_per_s = world * c["N"] * c["B"] / (ms_step * 1e-3)
 
     # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
     x_host = xsrc.cpu().pin_memory()
@@ -411,7 +443,8 @@ def run_tcbf(args, c):
                    "l2": ("flushed between steps (256 MiB write)" if flush else
                           f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
                    "parallelism": f"batch-sharded x{world}, no data-path collective",
-                   "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4)},
+                   "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4),
+                   "samples_per_s": round(frames_per_s, 1)},
         "roofline": roof,
         "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s", "h2d_bytes_per_step": int(x_host.numel() * 4),
                 "d2h_bytes_per_step": int(plan.out_bytes), "api": "tcbf_beamform_host (pinned host buffers)",

@@ -146,10 +146,12 @@ def _lib():
     return _LIB
 
 
-def generate_device(dist, seed: int, tensor_id: int, B: int, R: int, C: int, device="cuda", b0: int = 0):
+def generate_device(dist, seed: int, tensor_id: int, B: int, R: int, C: int, device="cuda", b0: int = 0,
+                    offset_elems: int = None):
     """Same values as `generate(...)[b0:b0+B]` of a larger tensor (batch entries b0..b0+B-1 of
     the global index space), produced on the GPU into a torch float32 tensor [B][R][C][2]
-    (interleaved).  torch is plumbing here."""
+    (interleaved).  `offset_elems` (default b0*R*C) selects any contiguous run of the global
+    element index space, e.g. a row slice of a huge matrix.  torch is plumbing here."""
     import torch
     if isinstance(dist, str):
         dist = DIST_NAMES[dist]
@@ -158,7 +160,8 @@ def generate_device(dist, seed: int, tensor_id: int, B: int, R: int, C: int, dev
     stream = torch.cuda.current_stream(out.device).cuda_stream
     rc = _lib().synth_generate_dev(ctypes.c_void_p(out.data_ptr()), int(dist),
                                    ctypes.c_uint64(stream_base(seed, tensor_id)),
-                                   B, R, C, int(b0) * R * C, ctypes.c_void_p(tab.data_ptr()),
+                                   B, R, C, int(b0) * R * C if offset_elems is None else int(offset_elems),
+                                   ctypes.c_void_p(tab.data_ptr()),
                                    ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"synth_generate_dev failed with cuda error {rc}")

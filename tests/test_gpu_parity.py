@@ -463,6 +463,36 @@ def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
                batches=[0, 200, 255], rows=[0, 63, 64, 777, 1023])
 
 
+def test_sliced_weight_generation_equals_direct(tcbf):
+    """bench.pack_weights' row-sliced generate+pack (for model matrices too large for one fp32
+    source) produces exactly the directly packed weights."""
+    import bench
+    c = dict(bench.CONFIGS["ultrasound_b1_planes"], M=1000, K=3000, N=64)
+    seed = synth.SEED_BASE + 3
+    plan = tcbf.Plan(c["M"], c["N"], c["K"], 1, "b1")
+    direct = plan.pack(tcbf.WEIGHTS, synth.generate_device(c["wd"], seed, 0, 1, c["M"], c["K"]))
+    sliced = bench.pack_weights(plan, c, seed, torch.device("cuda"), 0, max_src_bytes=300 * 3000 * 8)
+    assert torch.equal(direct, sliced)
+
+
+def test_full_size_ultrasound_b1_planes_sampled(tcbf):
+    """The ultrasound 1-bit pipeline shape: M=49152, K=262144, N=1024, with the
+    weights generated and packed in slices exactly as bench.py does; sampled beams vs the oracle."""
+    import bench
+    c = bench.CONFIGS["ultrasound_b1_planes"]
+    M, N, K = c["M"], c["N"], c["K"]
+    seed = synth.SEED_BASE + c["idx"]
+    plan = tcbf.Plan(M, N, K, 1, "b1")
+    wp = bench.pack_weights(plan, c, seed, torch.device("cuda"), 0)
+    y = plan.beamform_raw(wp, synth.generate_device(c["xd"], seed, 1, 1, K, N))
+    torch.cuda.synchronize()
+    rows = [0, 20000, 49151]
+    w = synth.generate(c["wd"], seed, 0, 1, M, K, r_sel=rows)
+    x = synth.generate(c["xd"], seed, 1, 1, K, N)
+    ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, len(rows), N, K, 1)
+    assert np.array_equal(y[0][:, rows].cpu().numpy()[None], ref)
+
+
 def test_full_size_ultrasound_f16_sampled(tcbf):
     """BASELINE configs[3]: M=65536, K=8192, N=256, batch=8 (17 GB of packed weights)."""
     _full_size(tcbf, "f16", 65536, 256, 8192, 8, "phase_amp", "adc_scaled", synth.SEED_BASE + 3,
