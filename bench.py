@@ -426,7 +426,8 @@ def run_tcbf(args, c):
     roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
                         fused=fused)
     roof["traffic"] = traffic_for(args.config, plan.variant)
-    roof["kernel"] = "f16_tcgen05_fused_pack_bres_128x128" if fused else plan.variant
+    roof["kernel"] = (("f16_tcgen05_fused_pack_bres_128x128" if plan.k_packed <= 256 else
+                       "f16_tcgen05_stream_conv_128x128") if fused else plan.variant)
     roof["kernel_ms"] = round(gemm_ms_max, 4)
     roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
     roof["useful_ops_per_launch"] = useful_ops(c)

@@ -96,6 +96,11 @@ def layout_sizes(M, N, K, batch, precision="f16"):
     return w.value, x.value, o.value, k.value
 
 
+def _num_sms():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
 def _stream_ptr(stream, device):
     import torch
     if stream is None:
@@ -176,7 +181,10 @@ class Plan:
     @property
     def raw_fused(self) -> bool:
         """True when beamform_raw runs the fused single-kernel path for this plan."""
-        return self.precision == F16 and self.k_packed <= 256 and self.N % 4 == 0
+        if self.precision != F16 or self.N % 4:
+            return False
+        tiles = (self.N + 127) // 128 * self.batch
+        return self.k_packed <= 256 or (self.M <= 128 and tiles >= _num_sms() // 2)
 
     def steering_weights(self, positions, angles, freqs, c, layout="interleaved", out=None, stream=None):
         """fp32 weight source w[b][m][k] = exp(+2 pi i f_b d_k sin(theta_m) / c).

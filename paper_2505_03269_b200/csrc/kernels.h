@@ -40,6 +40,9 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
                             cudaStream_t stream);
 
 bool gemm_f16_fused_supported(int64_t K16, int64_t N);
+int gemm_f16_conv_block_k();
+cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
+                                 const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 

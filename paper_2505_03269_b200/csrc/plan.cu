@@ -403,6 +403,37 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     g_launches = 1;
     return TCBF_OK;
   }
+  // Small-M plans (one 128-row weight tile): every data element enters one tile, so the
+  // streaming kernel converts the fp32 data on the fly (no separate pack pass).
+  // Needs enough (batch, column) tiles to occupy the GPU (measured: 32 tiles lose to pack + GEMM).
+  bool stream_conv = plan->prec == TCBF_PREC_F16 && plan->M <= 128 && plan->N % 4 == 0 &&
+                     ((plan->N + 127) / 128) * plan->B >= plan->num_sms / 2;
+  if (const char* env = getenv("TCBF_NO_FUSED")) stream_conv = stream_conv && atoi(env) == 0;
+  if (stream_conv) {
+    const int bk = tcbf::gemm_f16_conv_block_k();
+    CUtensorMap ta, tc;
+    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
+                  CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 128,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = 1;
+    a.tiles_n = (int)((plan->N + 127) / 128);
+    a.group_m = 1;
+    const int64_t nt = (int64_t)a.tiles_n * plan->B;
+    if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+    a.num_tiles = (int)nt;
+    a.num_kb = (int)(plan->kp / bk);
+    a.out = static_cast<float*>(out);
+    cudaError_t e = tcbf::launch_gemm_f16_conv(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "streaming-conversion beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, plan->x_bytes, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (data scratch)");

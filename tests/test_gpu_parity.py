@@ -211,7 +211,10 @@ RAW_SHAPES = [
     (256, 256, 256, 2, "interleaved"),   # fused, vector loads, exactly K16 = 256
     (130, 136, 64, 3, "planar"),         # fused, planar source
     (8, 64, 32, 2, "interleaved"),       # tiny (BASELINE configs[0])
-    (64, 96, 300, 2, "interleaved"),     # K16 = 320 > 256 -> pack + beamform fallback
+    (64, 96, 300, 2, "interleaved"),     # K16 = 320 > 256, M <= 128 -> streaming-conversion kernel
+    (32, 1024, 5000, 1, "interleaved"),  # M=32 sweep shape class, long K, streaming conversion
+    (100, 260, 700, 2, "planar"),        # streaming conversion, planar, ragged N (scalar loads)
+    (300, 96, 300, 2, "interleaved"),    # M > 128 and K16 > 256 -> pack + beamform fallback
     (70, 77, 40, 2, "interleaved"),      # N % 4 != 0 -> fallback
 ]
 
