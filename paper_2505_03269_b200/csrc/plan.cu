@@ -407,7 +407,7 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   // streaming kernel converts the fp32 data on the fly (no separate pack pass).
   // Needs enough (batch, column) tiles to occupy the GPU (measured: 32 tiles lose to pack + GEMM).
   bool stream_conv = plan->prec == TCBF_PREC_F16 && plan->M <= 128 && plan->N % 4 == 0 &&
-                     ((plan->N + 127) / 128) * plan->B >= plan->num_sms / 2;
+                     (((plan->N + 127) / 128) * plan->B >= plan->num_sms / 2 || getenv("TCBF_FORCE_STREAM_CONV"));
   if (const char* env = getenv("TCBF_NO_FUSED")) stream_conv = stream_conv && atoi(env) == 0;
   if (stream_conv) {
     const int bk = tcbf::gemm_f16_conv_block_k();

@@ -219,8 +219,15 @@ RAW_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("shape", RAW_SHAPES)
-def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape):
+@pytest.fixture(params=["auto", "force_stream"])
+def raw_mode(request, monkeypatch):
+    if request.param == "force_stream":   # small-M shapes through the streaming-conversion kernel
+        monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
+    return request.param
+
+
+@pytest.mark.parametrize("shape", RAW_SHAPES + [(32, 256, 1000, 80, "interleaved")])  # 160 tiles: streams
+def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode):
     M, N, K, B, layout = shape
     w = synth.generate("phase", 17, 0, B, M, K)
     x = synth.generate("adc", 17, 1, B, K, N)
