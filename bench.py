@@ -120,14 +120,15 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
                 frac=round(ach / tpeak, 4), peak_src=src, hbm_frac=round(byts / t_ms / 1e9 / bw, 4))
 
 
-def traffic_for(c_name, variant):
-    """dram bytes per launch from the committed ncu --set full capture (profiles/), or None."""
+def traffic_for(c_name, kernel):
+    """dram bytes per launch from the committed ncu --set full capture (profiles/traffic.json) of
+    the same config and kernel, or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
         e = d.get(c_name)
-        if e and e.get("variant") == variant:
+        if e and e.get("kernel") == kernel:
             return e.get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -425,9 +426,9 @@ def run_tcbf(args, c):
     peaks = load_peaks()
     roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
                         fused=fused)
-    roof["traffic"] = traffic_for(args.config, plan.variant)
     roof["kernel"] = (("f16_tcgen05_fused_pack_bres_128x128" if plan.k_packed <= 256 else
                        "f16_tcgen05_stream_conv_128x128") if fused else plan.variant)
+    roof["traffic"] = traffic_for(args.config, roof["kernel"])
     roof["kernel_ms"] = round(gemm_ms_max, 4)
     roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
     roof["useful_ops_per_launch"] = useful_ops(c)
