@@ -160,7 +160,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   else if (M <= 128 || N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
   else if (K >= 2048 && N >= 256) p->f16_variant = tcbf::F16_V_2CTA_N256;   // long K: compute-bound
   else if (kp > 256) p->f16_variant = tcbf::F16_V_2CTA_N128;              // mid K (measured +5-8%)
-  else p->f16_variant = tcbf::F16_V_K64_S3_COOP;                          // short K: store-bound
+  else p->f16_variant = tcbf::F16_V_K64_S3;                               // short K: store-bound
   if (const char* env = getenv("TCBF_F16_VARIANT")) {
     int v = atoi(env);
     if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
