@@ -181,7 +181,10 @@ class Plan:
     @property
     def raw_fused(self) -> bool:
         """True when beamform_raw runs the fused single-kernel path for this plan."""
-        if self.precision != F16 or self.N % 4:
+        if self.precision == B1:   # fused 1-bit kernel is opt-in (TCBF_B1_FUSED=1)
+            return (self.k_packed <= 16 and self.N % 4 == 0 and os.environ.get("TCBF_B1_KERNEL", "i8") == "i8"
+                    and "TCBF_B1_FUSED" in os.environ)
+        if self.N % 4:
             return False
         tiles = (self.N + 127) // 128 * self.batch
         return self.k_packed <= 256 or (self.M <= 128 and tiles >= _num_sms() // 2)

@@ -403,6 +403,27 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     g_launches = 1;
     return TCBF_OK;
   }
+  // 1-bit fused kernel (data quantised + packed inside the GEMM): bit-exact but measured slower
+  // than pack + GEMM on radio b1 (4.4 vs 2.8 ms: its converters cannot keep enough loads in
+  // flight beside the expanded stages), so it is opt-in.
+  bool b1_fused = plan->prec == TCBF_PREC_B1 && plan->b1_tc == 1 &&
+                  tcbf::gemm_b1_fused_supported(plan->kp, plan->N) && getenv("TCBF_B1_FUSED") != nullptr;
+  if (b1_fused) {
+    CUtensorMap tc;
+    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmB1Args a;
+    memset(&a, 0, sizeof(a));
+    a.w = static_cast<const uint32_t*>(w_packed);
+    a.out = static_cast<int32_t*>(out);
+    a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
+    a.splits = 1;
+    cudaError_t e = tcbf::launch_gemm_b1_fused(tc, a, x_src, (int)layout, plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused 1-bit beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
   // Small-M plans (one 128-row weight tile): every data element enters one tile, so the
   // streaming kernel converts the fp32 data on the fly (no separate pack pass).
   // Needs enough (batch, column) tiles to occupy the GPU (measured: 32 tiles lose to pack + GEMM).

@@ -243,6 +243,47 @@ def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode):
     _check_f16(y_raw.cpu().numpy(), ref, w, x)
 
 
+@pytest.mark.parametrize("shape", [(70, 44, 300, 2), (200, 260, 512, 3), (8, 64, 32, 2), (130, 132, 33, 2),
+                                   (300, 1000, 480, 1)])
+@pytest.mark.parametrize("layout", ["interleaved", "planar"])
+def test_b1_beamform_raw_fused_bit_exact(tcbf, shape, layout, monkeypatch):
+    """1-bit fused path (opt-in; K <= 512, N % 4 == 0): fp32 data quantised and packed inside the
+    GEMM; bit-identical to pack + beamform and to the oracle."""
+    monkeypatch.setenv("TCBF_B1_FUSED", "1")
+    M, N, K, B = shape
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    w = synth.generate("adc", 19, 0, B, M, K)   # exact zeros exercise the >= 0 rule
+    x = synth.generate("adc", 19, 1, B, K, N)
+    plan = tcbf.Plan(M, N, K, B, "b1")
+    assert plan.raw_fused
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
+    xd = _dev(conv(x))
+    y_raw = plan.beamform_raw(wp, xd, layout)
+    y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
+    torch.cuda.synchronize()
+    assert torch.equal(y_raw, y_ref)
+    lay = 0 if layout == "interleaved" else 1
+    assert np.array_equal(y_raw.cpu().numpy(), oracle.cgemm_b1(conv(w), conv(x), lay, M, N, K, B))
+
+
+def test_full_size_radio_b1_raw_sampled(tcbf, monkeypatch):
+    """BASELINE configs[2] through the (opt-in) fused 1-bit path."""
+    monkeypatch.setenv("TCBF_B1_FUSED", "1")
+    M, N, K, B = 1024, 4096, 512, 256
+    seed = synth.SEED_BASE + 2
+    plan = tcbf.Plan(M, N, K, B, "b1")
+    assert plan.raw_fused
+    wp = plan.pack(tcbf.WEIGHTS, synth.generate_device("phase", seed, 0, B, M, K))
+    y = plan.beamform_raw(wp, synth.generate_device("adc", seed, 1, B, K, N))
+    torch.cuda.synchronize()
+    rows = [0, 129, 1023]
+    for b in (0, 100, 255):
+        w = synth.generate("phase", seed, 0, B, M, K, b_sel=[b], r_sel=rows)
+        x = synth.generate("adc", seed, 1, B, K, N, b_sel=[b])
+        ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, len(rows), N, K, 1)
+        assert np.array_equal(y[b][:, rows].cpu().numpy()[None], ref)
+
+
 def test_b1_beamform_raw_falls_back_bit_exact(tcbf):
     M, N, K, B = 70, 45, 300, 2
     w = synth.generate("adc", 5, 0, B, M, K)
