@@ -464,7 +464,9 @@ def run_tcbf(args, c):
         j = max_over_ranks(j, dev) if world == 1 else j
         line["energy"] = {"joules_per_step": round(j / args.steps, 6),
                           "teraops_per_joule": round(useful_ops(c) / (j / args.steps) / 1e12, 3),
-                          "source": "NVML total energy counter, this GPU, timed region"}
+                          "timed_region_s": round(total_ms / 1e3, 3),
+                          "source": "NVML total energy counter, this GPU, timed region "
+                                    "(counter granularity makes regions < ~1 s coarse)"}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c)
     if rank == 0:

@@ -6,6 +6,7 @@
 // once, the measurement matrix per ensemble).  Each chunk runs tcbf_beamform_raw.
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstring>
 
 #include "plan_internal.h"
@@ -26,6 +27,16 @@ extern "C" tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_p
   if (cb > B) cb = B;
   const int64_t nchunks = (B + cb - 1) / cb;
 
+  // Keep the stream-ordered pool's memory between calls (the default release threshold of 0
+  // would hand the scratch back to the driver at every synchronize and re-allocate each call).
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   cudaStream_t st[2] = {nullptr, nullptr};
   void* buf[2] = {nullptr, nullptr};
   tcbf_status status = TCBF_OK;
