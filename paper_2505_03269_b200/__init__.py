@@ -96,6 +96,14 @@ def layout_sizes(M, N, K, batch, precision="f16"):
     return w.value, x.value, o.value, k.value
 
 
+def _conv_splits(tiles, num_kb, num_sms):
+    """K split of the streaming-conversion kernel (mirror of gemm_f16_conv_splits in gemm_f16_conv.cu)."""
+    if tiles <= 0 or num_sms <= 0 or tiles * 5 >= num_sms * 3:
+        return 1
+    s = (num_sms * 85 // 100 + tiles - 1) // tiles
+    return max(1, min(s, 16, num_kb // 16))
+
+
 def _num_sms():
     import torch
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
@@ -186,8 +194,11 @@ class Plan:
                     and "TCBF_B1_FUSED" in os.environ)
         if self.N % 4:
             return False
+        if self.k_packed <= 256:
+            return True
         tiles = (self.N + 127) // 128 * self.batch
-        return self.k_packed <= 256 or (self.M <= 128 and tiles >= _num_sms() // 2)
+        units = tiles * _conv_splits(tiles, (self.K + 31) // 32, _num_sms())
+        return self.M <= 128 and (units >= _num_sms() // 4 or "TCBF_FORCE_STREAM_CONV" in os.environ)
 
     def steering_weights(self, positions, angles, freqs, c, layout="interleaved", out=None, stream=None):
         """fp32 weight source w[b][m][k] = exp(+2 pi i f_b d_k sin(theta_m) / c).

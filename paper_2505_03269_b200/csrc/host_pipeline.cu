@@ -29,14 +29,7 @@ extern "C" tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_p
 
   // Keep the stream-ordered pool's memory between calls (the default release threshold of 0
   // would hand the scratch back to the driver at every synchronize and re-allocate each call).
-  {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
+  retain_pool_memory();
   cudaStream_t st[2] = {nullptr, nullptr};
   void* buf[2] = {nullptr, nullptr};
   tcbf_status status = TCBF_OK;

@@ -13,6 +13,7 @@ struct GemmF16Args {
   float* out;  // used by the masked-store epilogue (N % 4 != 0)
   int debug;   // ablation (TCBF_DEBUG): bit0 skip output stores, bit1 skip MMAs
   int group_m; // tile rows per rasterisation group (tile_coords)
+  int splits, kb_per_split;  // K split of the streaming-conversion kernel (fp32 TMA reduce-add)
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
@@ -41,8 +42,9 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
 
 bool gemm_f16_fused_supported(int64_t K16, int64_t N);
 int gemm_f16_conv_block_k();
-cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
-                                 const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
+int gemm_f16_conv_splits(int tiles, int num_kb, int num_sms);
+cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
+                                 const GemmF16Args& args, int layout, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 

@@ -112,6 +112,19 @@ bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) %
 
 }  // namespace
 
+void retain_pool_memory() {
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+}
+
+namespace {
+
+}  // namespace
+
 void tcbf_internal_set_launches(int n) { g_launches = n; }
 
 extern "C" {
@@ -427,14 +440,29 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   // Small-M plans (one 128-row weight tile): every data element enters one tile, so the
   // streaming kernel converts the fp32 data on the fly (no separate pack pass).
   // Needs enough (batch, column) tiles to occupy the GPU (measured: 32 tiles lose to pack + GEMM).
-  bool stream_conv = plan->prec == TCBF_PREC_F16 && plan->M <= 128 && plan->N % 4 == 0 &&
-                     (((plan->N + 127) / 128) * plan->B >= plan->num_sms / 2 || getenv("TCBF_FORCE_STREAM_CONV"));
+  // Needs enough work units (column tiles x K splits) to occupy the GPU; below a quarter of the
+  // SMs the pack + GEMM pair is kept.
+  const int64_t conv_tiles = ((plan->N + 127) / 128) * plan->B;
+  const int conv_kb = (int)((plan->K + tcbf::gemm_f16_conv_block_k() - 1) / tcbf::gemm_f16_conv_block_k());
+  const int64_t conv_units =
+      conv_tiles * (conv_tiles < INT32_MAX ? tcbf::gemm_f16_conv_splits((int)conv_tiles, conv_kb, plan->num_sms) : 1);
+  bool stream_conv = plan->prec == TCBF_PREC_F16 && plan->M <= 128 && plan->N % 4 == 0 && aligned(x_src, 16) &&
+                     (conv_units >= plan->num_sms / 4 || getenv("TCBF_FORCE_STREAM_CONV"));
   if (const char* env = getenv("TCBF_NO_FUSED")) stream_conv = stream_conv && atoi(env) == 0;
   if (stream_conv) {
     const int bk = tcbf::gemm_f16_conv_block_k();
-    CUtensorMap ta, tc;
+    CUtensorMap ta, tx, tc;
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    // raw fp32 data: interleaved [B][K][2N] (box 256 floats = 128 complex x 32 k-rows) or planar
+    // [2B][K][N] (box 128 x 32 per plane); out-of-range k / n are zero-filled by the TMA unit
+    if (layout == TCBF_SRC_INTERLEAVED)
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x_src, 2 * plan->N, plan->K, plan->B, 256, bk,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    else
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x_src, plan->N, plan->K, 2 * plan->B, 128, bk,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
     s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 128,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
@@ -446,15 +474,28 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     a.tiles_n = (int)((plan->N + 127) / 128);
     a.group_m = 1;
     const int64_t nt = (int64_t)a.tiles_n * plan->B;
-    if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+    if (nt * 16 > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
     a.num_tiles = (int)nt;
-    a.num_kb = (int)(plan->kp / bk);
+    a.num_kb = (int)((plan->K + bk - 1) / bk);
+    a.splits = tcbf::gemm_f16_conv_splits(a.num_tiles, a.num_kb, plan->num_sms);
+    if (const char* env = getenv("TCBF_CONV_SPLITS")) a.splits = std::max(1, std::min(atoi(env), a.num_kb));
+    a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
+    a.splits = (a.num_kb + a.kb_per_split - 1) / a.kb_per_split;
     a.out = static_cast<float*>(out);
-    cudaError_t e = tcbf::launch_gemm_f16_conv(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    int launches = 1;
+    if (a.splits > 1) {  // partial sums are reduce-added into a zeroed output
+      cudaError_t e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
+      launches = 2;
+    }
+    cudaError_t e = tcbf::launch_gemm_f16_conv(ta, tx, tc, a, (int)layout, plan->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "streaming-conversion beamform kernel launch");
-    g_launches = 1;
+    g_launches = launches;
     return TCBF_OK;
   }
+  // Keep the stream-ordered pool's memory cached between calls (the default release threshold
+  // returns it to the driver at every synchronisation, making each call pay a fresh allocation).
+  retain_pool_memory();
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, plan->x_bytes, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (data scratch)");

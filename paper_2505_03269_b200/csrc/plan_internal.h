@@ -19,3 +19,5 @@ struct tcbf_plan_s {
 
 // launch accounting shared by the ABI entry points (thread-local in plan.cu)
 __attribute__((visibility("hidden"))) void tcbf_internal_set_launches(int n);
+// sets the current device's default mempool release threshold to "never" (stream-ordered scratch)
+__attribute__((visibility("hidden"))) void retain_pool_memory();

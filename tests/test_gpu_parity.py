@@ -227,7 +227,8 @@ def raw_mode(request, monkeypatch):
 
 
 @pytest.mark.parametrize("shape", RAW_SHAPES + [(32, 256, 1000, 80, "interleaved")])  # 160 tiles: streams
-def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode):
+def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode, monkeypatch):
+    monkeypatch.setenv("TCBF_CONV_SPLITS", "1")  # split-K sums in another order: tested below
     M, N, K, B, layout = shape
     w = synth.generate("phase", 17, 0, B, M, K)
     x = synth.generate("adc", 17, 1, B, K, N)
@@ -239,6 +240,35 @@ def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode):
     y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
     torch.cuda.synchronize()
     assert torch.equal(y_raw, y_ref)
+    ref = oracle.cgemm_f16(conv(w), conv(x), 0 if layout == "interleaved" else 1, M, N, K, B)
+    _check_f16(y_raw.cpu().numpy(), ref, w, x)
+
+
+@pytest.mark.parametrize("shape", [(32, 1024, 5000, 1, "interleaved"), (100, 260, 700, 2, "planar"),
+                                   (128, 512, 2049, 3, "interleaved"), (16, 128, 4096, 1, "planar")])
+@pytest.mark.parametrize("splits", ["auto", "3", "16"])
+def test_f16_beamform_raw_split_k(tcbf, shape, splits, monkeypatch):
+    """Streaming-conversion kernel with K split across CTAs (fp32 partial tiles reduce-added by
+    the TMA unit into the zeroed output): within the fp16 tolerance of the oracle and equal to
+    the packed path up to fp32 summation order."""
+    monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
+    if splits != "auto":
+        monkeypatch.setenv("TCBF_CONV_SPLITS", splits)
+    M, N, K, B, layout = shape
+    w = synth.generate("phase", 23, 0, B, M, K)
+    x = synth.generate("adc", 23, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
+    xd = _dev(conv(x))
+    y_raw = plan.beamform_raw(wp, xd, layout)
+    n_launch = tcbf.Plan.last_launch_count()
+    y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
+    torch.cuda.synchronize()
+    if splits != "auto":
+        assert n_launch == 2  # memset + kernel
+    scale = y_ref.abs().max().item()
+    assert (y_raw - y_ref).abs().max().item() <= 1e-4 * scale  # fp32 partial sums, another order
     ref = oracle.cgemm_f16(conv(w), conv(x), 0 if layout == "interleaved" else 1, M, N, K, B)
     _check_f16(y_raw.cpu().numpy(), ref, w, x)
 
