@@ -93,8 +93,8 @@ def load_peaks():
 def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
     """Dominant kernel = the beamform GEMM.  Binding roof = the slower of the HBM time
     (algorithmic bytes / measured copy bandwidth) and the tensor time (useful ops / peak):
-    fp16 tensor peak = measured bf16 peak (same nominal rate); the 1-bit tensor-core kernel
-    runs int8 MMAs whose nominal rate is 2x fp16 (guide ratio) -> 2 x measured bf16.  The
+    fp16 tensor peak = measured bf16 peak (same nominal rate); the 1-bit tensor-core kernels
+    run fp4 (default, 4x fp16 nominal) or int8 / fp8 MMAs (2x) -> 4x or 2x measured bf16.  The
     CUDA-core popc kernel (TCBF_B1_KERNEL=popc) reports 'alu' against 16 POPC/clk/SM."""
     ops = useful_ops(c)
     byts = gemm_bytes(c, fused)
@@ -105,18 +105,21 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
         ach = ops / t_ms / 1e12
         return dict(bound="alu", achieved=round(ach, 1), peak=round(alu_peak, 1), unit="TOP/s",
                     frac=round(ach / alu_peak, 4), peak_src="derived (16 POPC/clk/SM x 148 x 1965 MHz)")
-    ratio = 1.0 if c["prec"] == "f16" else 2.0
+    # fp16: 1x bf16; 1-bit on int8 MMAs (i8 / i8pair): 2x; on +-1 e4m3 (f8): 2x; on +-1 e2m1
+    # with unit block scales (mxf4): 4x -- B200 nominal dense 2.25 / 4.5 / 4.5 / 9 P(FL)OP/s
+    ratio = 1.0 if c["prec"] == "f16" else (4.0 if "mxf4" in variant else 2.0)
     base = peaks["bf16_sus"] if long_step else peaks["bf16"]
     tpeak = base * ratio
     t_hbm = byts / (bw * 1e9)
     t_tc = ops / (tpeak * 1e12)
-    src = peaks["src"] + (" sustained" if long_step else " burst") + ("" if ratio == 1 else " x2 (int8 nominal ratio)")
+    src = peaks["src"] + (" sustained" if long_step else " burst") + {
+        1.0: "", 2.0: " x2 (int8/fp8 nominal ratio)", 4.0: " x4 (fp4 nominal ratio)"}[ratio]
     if t_hbm >= t_tc:
         ach = byts / t_ms / 1e9
         return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
                     peak_src=peaks["src"], tensor_frac=round(ops / t_ms / 1e12 / tpeak, 4))
     ach = ops / t_ms / 1e12
-    return dict(bound="tensor", achieved=round(ach, 1), peak=round(tpeak, 1), unit="TOP/s" if ratio == 2 else "TFLOP/s",
+    return dict(bound="tensor", achieved=round(ach, 1), peak=round(tpeak, 1), unit="TOP/s" if ratio > 1 else "TFLOP/s",
                 frac=round(ach / tpeak, 4), peak_src=src, hbm_frac=round(byts / t_ms / 1e9 / bw, 4))
 
 

@@ -189,8 +189,8 @@ class Plan:
     @property
     def raw_fused(self) -> bool:
         """True when beamform_raw runs the fused single-kernel path for this plan."""
-        if self.precision == B1:   # fused 1-bit kernel is opt-in (TCBF_B1_FUSED=1)
-            return (self.k_packed <= 16 and self.N % 4 == 0 and os.environ.get("TCBF_B1_KERNEL", "i8") == "i8"
+        if self.precision == B1:   # fused 1-bit kernel: int8 variant, opt-in (TCBF_B1_FUSED=1, TCBF_B1_KERNEL=i8)
+            return (self.k_packed <= 16 and self.N % 4 == 0 and os.environ.get("TCBF_B1_KERNEL") == "i8"
                     and "TCBF_B1_FUSED" in os.environ)
         if self.N % 4:
             return False

@@ -21,7 +21,7 @@
 //     contribute; no K_pad term is needed.
 //
 // Roles (persistent CTA per SM, 416 threads):
-//   warp 0      TMEM allocator + single-thread MMA issuer (4 MMAs per K=32 step)
+//   warp 0      TMEM allocator + single-thread MMA issuer (2 MMAs of N = 256 per K=32 step)
 //   warps 1-4   epilogue: tcgen05.ld, + row term + column term (one IADD3), TMA store of int32
 //   warps 5-8   expanders for A_r, A_i (one weight row per thread; also |A_r| + |A_i|)
 //   warps 9-12  expanders for B_r, B_i, ~B_i (one data column per thread; also |B_r|, |B_i|)
@@ -41,7 +41,7 @@ constexpr int BN = 128;
 constexpr int KB_WORDS = 4;            // 128 bits per K block -> 128 expanded bytes per row
 constexpr int TILE_BYTES = 128 * 128;  // one expanded operand tile (rows x 128 B)
 constexpr int STAGES = 2;
-constexpr int STAGE_BYTES = 5 * TILE_BYTES;  // A_r, A_i, B_r, B_i, ~B_i
+constexpr int STAGE_BYTES = 5 * TILE_BYTES;  // A_r, A_i, ~B_i, B_r, B_i
 constexpr int EPI_BYTES = 4 * 2 * 4096;
 constexpr int COLSUM_BYTES = 2 * 3 * 128 * 4;  // [2 acc buf][|A_r|+|A_i| rows, |B_r|, |B_i| cols][128]
 constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES + COLSUM_BYTES;
@@ -132,8 +132,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      // kind::i8, unsigned A and B, int32 D, K-major, M = 128, N = BN
-      constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(BN >> 3) << 17) |
+      // kind::i8, unsigned A and B, int32 D, K-major, M = 128, N = 2 BN: one MMA covers both
+      // accumulators [D_r | D_i] (contiguous TMEM columns) against two stacked data tiles, so A
+      // is read from smem once per pair of sub-products (the stage holds ~B_i, B_r, B_i in row
+      // order: A_r x [B_r; B_i] and A_i x [~B_i; B_r])
+      constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) |
                                  ((uint32_t)(BM >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
@@ -144,29 +147,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int abuf = it & 1;
         mbar_wait(&tempty_bar[abuf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_re = tmem_base + abuf * 2 * BN;
-        const uint32_t d_im = d_re + BN;
+        const uint32_t d_re = tmem_base + abuf * 2 * BN;  // D_i follows at d_re + BN
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           uint8_t* st = smem + stage * STAGE_BYTES;
           uint8_t* sAr = st;
           uint8_t* sAi = st + TILE_BYTES;
-          uint8_t* sBr = st + 2 * TILE_BYTES;
-          uint8_t* sBi = st + 3 * TILE_BYTES;
-          uint8_t* sBc = st + 4 * TILE_BYTES;
+          uint8_t* sBc = st + 2 * TILE_BYTES;  // ~B_i, B_r, B_i: consecutive 128-row tiles
+          uint8_t* sBr = st + 3 * TILE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // K = 32 bytes per MMA
             const uint32_t off = kk * 32;
             const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
-            const uint64_t br = smem_desc_k128(sBr, off), bi = smem_desc_k128(sBi, off);
-            const uint64_t bc = smem_desc_k128(sBc, off);
+            const uint64_t b_ri = smem_desc_k128(sBr, off);  // [B_r; B_i]
+            const uint64_t b_cr = smem_desc_k128(sBc, off);  // [~B_i; B_r]
             const uint32_t acc = ((kb - kb0) | kk) ? 1u : 0u;
             if (p.debug & 2) continue;
-            mma_i8_ss(d_re, ar, br, IDESC, acc);  // P(A_r & B_r)
-            mma_i8_ss(d_re, ai, bc, IDESC, 1u);   // P(A_i & ~B_i)
-            mma_i8_ss(d_im, ar, bi, IDESC, acc);  // P(A_r & B_i)
-            mma_i8_ss(d_im, ai, br, IDESC, 1u);   // P(A_i & B_r)
+            mma_i8_ss(d_re, ar, b_ri, IDESC, acc);  // [P(A_r & B_r) | P(A_r & B_i)]
+            mma_i8_ss(d_re, ai, b_cr, IDESC, 1u);   // [P(A_i & ~B_i) | P(A_i & B_r)]
           }
           mma_commit(&empty_bar[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -339,9 +338,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           expand_word(ai, row, 0, wi.x); expand_word(ai, row, 1, wi.y);
           expand_word(ai, row, 2, wi.z); expand_word(ai, row, 3, wi.w);
         } else {
-          uint8_t* br = st + 2 * TILE_BYTES + row * 128;
-          uint8_t* bi = st + 3 * TILE_BYTES + row * 128;
-          uint8_t* bc = st + 4 * TILE_BYTES + row * 128;
+          uint8_t* bc = st + 2 * TILE_BYTES + row * 128;
+          uint8_t* br = st + 3 * TILE_BYTES + row * 128;
+          uint8_t* bi = st + 4 * TILE_BYTES + row * 128;
           expand_word(br, row, 0, wr.x); expand_word(br, row, 1, wr.y);
           expand_word(br, row, 2, wr.z); expand_word(br, row, 3, wr.w);
           expand_word_pair(bi, bc, row, 0, wi.x); expand_word_pair(bi, bc, row, 1, wi.y);

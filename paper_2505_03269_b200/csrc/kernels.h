@@ -62,6 +62,12 @@ cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_2cta(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
                                 cudaStream_t stream);
 bool gemm_b1_f8_supported(int64_t Kw);
+bool gemm_b1_f4_supported(int64_t Kw);
+int gemm_b1_f4_block_words();
+bool gemm_b1_f4_tma_words(int64_t Kw);
+int gemm_b1_f4_store_box_cols(int64_t Kw);
+cudaError_t launch_gemm_b1_f4(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
+                              const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
 bool gemm_b1_fused_supported(int64_t Kw, int64_t N);
 cudaError_t launch_gemm_b1_fused(const CUtensorMap& tmC, const GemmB1Args& args, const float* x_src, int layout,
                                  int num_sms, cudaStream_t stream);

@@ -280,6 +280,7 @@ def test_b1_beamform_raw_fused_bit_exact(tcbf, shape, layout, monkeypatch):
     """1-bit fused path (opt-in; K <= 512, N % 4 == 0): fp32 data quantised and packed inside the
     GEMM; bit-identical to pack + beamform and to the oracle."""
     monkeypatch.setenv("TCBF_B1_FUSED", "1")
+    monkeypatch.setenv("TCBF_B1_KERNEL", "i8")  # the fused data-pack kernel is an int8 variant
     M, N, K, B = shape
     conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
     w = synth.generate("adc", 19, 0, B, M, K)   # exact zeros exercise the >= 0 rule
@@ -299,6 +300,7 @@ def test_b1_beamform_raw_fused_bit_exact(tcbf, shape, layout, monkeypatch):
 def test_full_size_radio_b1_raw_sampled(tcbf, monkeypatch):
     """BASELINE configs[2] through the (opt-in) fused 1-bit path."""
     monkeypatch.setenv("TCBF_B1_FUSED", "1")
+    monkeypatch.setenv("TCBF_B1_KERNEL", "i8")  # the fused data-pack kernel is an int8 variant
     M, N, K, B = 1024, 4096, 512, 256
     seed = synth.SEED_BASE + 2
     plan = tcbf.Plan(M, N, K, B, "b1")
@@ -428,10 +430,10 @@ def test_abi_errors_on_device(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
-@pytest.fixture(params=["f8", "i8", "i8pair", "popc"])
+@pytest.fixture(params=["f4", "f8", "i8", "i8pair", "popc"])
 def b1_kernel(request, monkeypatch):
-    """All 1-bit kernels: tcgen05 kind::f8f6f4 on +-1 (default), tcgen05 kind::i8 AND form,
-    and the CUDA-core XOR/popc kernel."""
+    """All 1-bit kernels: tcgen05 kind::mxf4 and kind::f8f6f4 on +-1, tcgen05 kind::i8 AND form
+    (default; 1-CTA and CTA pair), and the CUDA-core XOR/popc kernel."""
     monkeypatch.setenv("TCBF_B1_KERNEL", request.param)
     return request.param
 
@@ -445,7 +447,8 @@ def test_b1_beamform_bit_exact(tcbf, shape, b1_kernel):
     M, N, K, B = shape
     w = synth.generate("adc", 31, 0, B, M, K)
     x = synth.generate("adc", 31, 1, B, K, N)
-    _, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    assert {"f4": "mxf4", "f8": "f8pm1", "i8pair": "2cta", "popc": "popc"}.get(b1_kernel, "i8") in plan.variant
     ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
     assert np.array_equal(y, ref)
     refp = oracle.cgemm_b1_packed(wp.cpu().numpy().view(np.uint32), xp.cpu().numpy().view(np.uint32),
@@ -482,6 +485,7 @@ def test_b1_random_corpus(tcbf, b1_kernel):
 def test_b1_split_k_bit_exact(tcbf, monkeypatch, splits):
     """Split-K (int8 kernel, TMA reduce-add of exact int32 partials): the M=32 sweep shape class
     and a ragged-N shape (atomic masked path), forced split counts included."""
+    monkeypatch.setenv("TCBF_B1_KERNEL", "i8")
     if splits != "auto":
         monkeypatch.setenv("TCBF_B1_SPLITS", splits)
     for (M, N, K, B) in [(32, 512, 4096 + 5, 1), (40, 77, 3000, 2)]:

@@ -23,7 +23,7 @@ SHAPES = [  # name, prec, M, N, K, B, wdist, xdist
     ("square_b1_8192", "b1", 8192, 8192, 8192, 1, "uniform", "uniform"),
 ]
 F16_VARIANTS = {"1cta_k64s3": "1", "1cta_coop": "11", "1cta_k32s4e8": "0", "2cta_256x128": "7", "2cta_256x256": "8"}
-B1_VARIANTS = ["i8", "f8", "i8pair"]
+B1_VARIANTS = ["f4", "i8", "f8", "i8pair"]
 
 
 def energy_mj():
