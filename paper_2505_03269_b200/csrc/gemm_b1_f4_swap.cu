@@ -1,0 +1,375 @@
+// gemm_b1_f4_swap.cu -- 1-bit-mode beamformer GEMM for few beams (M <= 64) on the fp4 tensor
+// cores, with the operand roles swapped.
+//
+// Same arithmetic as gemm_b1_f4.cu (+-1 e2m1 nibbles from the packed sign bits, kind::mxf4 with
+// unit block scales, exact fp32 accumulation, Im - 2 K_pad),
+// but the 128-row MMA dimension runs over the DATA columns and the beams form the MMA N
+// dimension, so a 32-beam plan does not pad its weights to 128 MMA rows (4x the tensor work) --
+// the small-beam sweep of BASELINE config 5.  With lanes = samples n and columns = beams m:
+//     [D_r^T | D_i^T] += X_r [W_r ; W_i]^T      [D_r^T | D_i^T] += X_i [-W_i ; W_r]^T
+// (the weights' stacked tiles -W_i, W_r, W_i are expanded once per K block; N = 2 TM).
+//
+// Tile = 128 samples x TM beams (TM = 32 or 64); TMEM holds two accumulator buffers of 2 TM
+// columns plus the scale-factor columns, so the epilogue of one tile overlaps the next tile's
+// MMAs.  The epilogue writes the transposed accumulator back as [m][n] rows: each lane holds one
+// sample n, so a warp's 32 lanes write 128 contiguous bytes of one beam row.
+//
+// Roles (persistent CTA per SM):
+//   warp 0        TMEM allocator + single-thread MMA issuer
+//   warps 1-4     epilogue (TMEM lane quarters), 32 x 32 TMA store boxes
+//   warps 5-8     expanders of X_r, X_i (one sample per thread)
+//   warps 9..     expanders of -W_i, W_r, W_i (one beam per thread; TM / 32 warps)
+//   last warp     TMA producer of the packed words
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tcbf {
+namespace {
+
+constexpr int TN = 128;  // samples per tile (MMA M)
+constexpr int KBW = 8;   // 256-bit K blocks -> 128-byte rows of nibbles
+constexpr int EPI_WARPS = 4;
+constexpr int XEXP_WARPS = 4;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t SF_COL = 256;
+
+template <int TM>
+struct SwapCfg {
+  static constexpr int X_TILE = TN * 128;                // one expanded data plane
+  static constexpr int W_TILE = TM * 128;                // one expanded weight plane
+  static constexpr int STAGE_BYTES = 2 * X_TILE + 3 * W_TILE;  // X_r, X_i, -W_i, W_r, W_i
+  static constexpr int STAGES = TM == 32 ? 3 : 2;
+  static constexpr int P_PLANE_X = TN * KBW * 4;         // packed words: 128 rows x 32 B
+  static constexpr int P_PLANE_W = TM * KBW * 4;
+  static constexpr int P_STAGE_BYTES = 2 * P_PLANE_X + 2 * P_PLANE_W;
+  static constexpr int P_STAGES = 4;
+  static constexpr int EPI_BYTES = EPI_WARPS * 2 * 4096;
+  static constexpr int P_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int EPI_OFFSET = P_OFFSET + P_STAGES * P_STAGE_BYTES;
+  static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
+  static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+  static constexpr int WEXP_WARPS = TM / 32;
+  static constexpr int EXP_WARPS = XEXP_WARPS + WEXP_WARPS;
+  static constexpr int EXP_WARP0 = 1 + EPI_WARPS;
+  static constexpr int PRODUCER_WARP = EXP_WARP0 + EXP_WARPS;
+  static constexpr int NUM_THREADS = (PRODUCER_WARP + 1) * 32;
+  static_assert(SMEM_BYTES <= 232448, "smem budget");
+  static_assert(2 * TM * 2 <= 256, "two accumulator buffers below the scale-factor columns");
+};
+
+template <int J>
+__device__ __forceinline__ uint32_t nib_pm1(uint32_t w) {
+  return ((w << (3 - J)) & 0x88888888u) ^ 0xAAAAAAAAu;  // bit 1 -> 0x2 (+1), bit 0 -> 0xA (-1)
+}
+template <int J>
+__device__ __forceinline__ uint32_t nib_neg(uint32_t w) {
+  return ((w << (3 - J)) & 0x88888888u) ^ 0x22222222u;  // bit 1 -> 0xA (-1), bit 0 -> 0x2 (+1)
+}
+__device__ __forceinline__ void put(uint8_t* row_base, int row, int q, uint4 v) {
+  *reinterpret_cast<uint4*>(row_base + ((q ^ (row & 7)) << 4)) = v;  // 128-byte swizzle
+}
+__device__ __forceinline__ void expand(uint8_t* row_base, int row, const uint4& lo, const uint4& hi) {
+  const uint32_t w[KBW] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+  for (int q = 0; q < KBW; ++q)
+    put(row_base, row, q, make_uint4(nib_pm1<0>(w[q]), nib_pm1<1>(w[q]), nib_pm1<2>(w[q]), nib_pm1<3>(w[q])));
+}
+__device__ __forceinline__ void expand_pair(uint8_t* pos_base, uint8_t* neg_base, int row, const uint4& lo,
+                                            const uint4& hi) {
+  const uint32_t w[KBW] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+  for (int q = 0; q < KBW; ++q) {
+    put(pos_base, row, q, make_uint4(nib_pm1<0>(w[q]), nib_pm1<1>(w[q]), nib_pm1<2>(w[q]), nib_pm1<3>(w[q])));
+    put(neg_base, row, q, make_uint4(nib_neg<0>(w[q]), nib_neg<1>(w[q]), nib_neg<2>(w[q]), nib_neg<3>(w[q])));
+  }
+}
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_same(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+      "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+
+// tile t -> (batch, sample tile, beam tile); beam tiles innermost (the weights stay in L2)
+__device__ __forceinline__ void swap_coords(int t, int tiles_m, int tiles_n, int& b, int& nt, int& mt) {
+  const int per_b = tiles_m * tiles_n;
+  b = t / per_b;
+  const int r = t - b * per_b;
+  nt = r / tiles_m;
+  mt = r - nt * tiles_m;
+}
+
+template <int TM, bool TMA_STORE>
+__global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
+    cgemm_b1_f4_swap_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                            const __grid_constant__ CUtensorMap tmC, GemmB1Args p, int tiles_m, int tiles_n,
+                            int num_tiles) {
+  using C = SwapCfg<TM>;
+  constexpr int STAGES = C::STAGES, P_STAGES = C::P_STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* packed = smem + C::P_OFFSET;
+  uint8_t* epi_base = smem + C::EPI_OFFSET;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::BAR_OFFSET);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* pfull = empty_bar + STAGES;
+  uint64_t* pempty = pfull + P_STAGES;
+  uint64_t* tfull = pempty + P_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_kb = p.Kw / KBW;
+  const int two_kpad = 2 * (32 * p.Kw - p.K);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], C::EXP_WARPS);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&pfull[s], 1);
+      mbar_init(&pempty[s], C::EXP_WARPS);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], EPI_WARPS);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    if (TMA_STORE) tma_prefetch_desc(&tmC);
+  }
+  if (warp == 0) {
+    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if (warp >= 1 && warp <= EPI_WARPS) {  // unit block scales: every byte of columns 256..511 = 0x7F
+    const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
+#pragma unroll
+    for (uint32_t c = SF_COL; c < TMEM_COLS; c += 32) tmem_st_same(tmem_base + lanes + c, 0x7F7F7F7Fu);
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // kind::mxf4 block32: e2m1 A/B, UE8M0 scales, fp32 D, K-major, M = 128 samples, N = 2 TM
+      constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * TM) >> 3) << 17) | (1u << 23) |
+                                 ((uint32_t)(TN >> 4) << 24);
+      const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + 128;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + abuf * 2 * TM;  // [D_r^T | D_i^T]
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * C::STAGE_BYTES;
+          uint8_t* sXr = st;
+          uint8_t* sXi = st + C::X_TILE;
+          uint8_t* sWn = st + 2 * C::X_TILE;   // -W_i, W_r, W_i: consecutive TM-row tiles
+          uint8_t* sWr = sWn + C::W_TILE;
+#pragma unroll
+          for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements (32 bytes) per MMA
+            const uint32_t off = kk * 32;
+            const uint64_t xr = smem_desc_k128(sXr, off), xi = smem_desc_k128(sXi, off);
+            const uint64_t w_ri = smem_desc_k128(sWr, off);  // [W_r; W_i]
+            const uint64_t w_nr = smem_desc_k128(sWn, off);  // [-W_i; W_r]
+            const uint32_t acc = (kb | kk) ? 1u : 0u;
+            if (p.debug & 2) continue;
+            mma_mxf4(d, xr, w_ri, IDESC, sfa, sfb, acc);
+            mma_mxf4(d, xi, w_nr, IDESC, sfa, sfb, 1u);
+          }
+          mma_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[abuf]);
+      }
+    }
+  } else if (warp <= EPI_WARPS) {
+    // ------------------------------------------------------------ epilogue (lane = sample)
+    const int q = warp & 3;
+    uint8_t* bufs = epi_base + (warp - 1) * 2 * 4096;
+    int sbuf = 0;
+    int it = 0;
+    constexpr int CHUNKS = 2 * TM / 32;  // 32-beam column chunks: Re parts, then Im parts
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      int b, nt, mt;
+      swap_coords(t, tiles_m, tiles_n, b, nt, mt);
+      const int n = nt * TN + q * 32 + lane;
+      const int abuf = it & 1;
+      mbar_wait(&tfull[abuf], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * TM;
+      uint32_t vbuf[2][32];
+      tmem_ld_32x32b_x32(tbase, vbuf[0]);
+#pragma unroll
+      for (int c = 0; c < CHUNKS; ++c) {
+        const int part = c / (TM / 32);
+        const int m0 = mt * TM + (c % (TM / 32)) * 32;
+        tmem_wait_ld();
+        if (c + 1 < CHUNKS) {
+          tmem_ld_32x32b_x32(tbase + (c + 1) * 32, vbuf[(c + 1) & 1]);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[abuf]);
+        }
+        uint32_t* vv = vbuf[c & 1];
+        const int corr = part == 0 ? 0 : two_kpad;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
+        if (p.debug & 1) continue;
+        if constexpr (TMA_STORE) {  // box of 32 beams x 32 samples, row = beam (128 B)
+          uint8_t* buf = bufs + sbuf * 4096;
+          if (lane == 0) bulk_wait_group_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) *reinterpret_cast<uint32_t*>(buf + j * 128 + lane * 4) = vv[j];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tmC, buf, nt * TN + q * 32, m0, 2 * b + part);
+            bulk_commit_group();
+          }
+          sbuf ^= 1;
+        } else if (n < p.N) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int m = m0 + j;
+            if (m < p.M) p.out[((size_t)(2 * b + part) * p.M + m) * (size_t)p.N + n] = (int32_t)vv[j];
+          }
+        }
+      }
+    }
+    if constexpr (TMA_STORE) {
+      if (lane == 0) bulk_wait_group<0>();
+      __syncwarp();
+    }
+  } else if (warp < C::PRODUCER_WARP) {
+    // ------------------------------------------------------------ expanders
+    const int e = threadIdx.x - C::EXP_WARP0 * 32;
+    const bool x_side = e < TN;
+    const int row = x_side ? e : e - TN;
+    int stage = 0, ps = 0;
+    uint32_t phase = 0, pph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&pfull[ps], pph);
+        const uint8_t* pk = packed + ps * C::P_STAGE_BYTES;
+        const uint8_t* pr = x_side ? pk + row * 32 : pk + 2 * C::P_PLANE_X + row * 32;
+        const int plane = x_side ? C::P_PLANE_X : C::P_PLANE_W;
+        const uint4 r0 = *reinterpret_cast<const uint4*>(pr);
+        const uint4 r1 = *reinterpret_cast<const uint4*>(pr + 16);
+        const uint4 i0 = *reinterpret_cast<const uint4*>(pr + plane);
+        const uint4 i1 = *reinterpret_cast<const uint4*>(pr + plane + 16);
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* st = smem + stage * C::STAGE_BYTES;
+        if (!(p.debug & 4)) {
+          if (x_side) {
+            expand(st + row * 128, row, r0, r1);
+            expand(st + C::X_TILE + row * 128, row, i0, i1);
+          } else {
+            uint8_t* wn = st + 2 * C::X_TILE;
+            expand(wn + C::W_TILE + row * 128, row, r0, r1);                          // W_r
+            expand_pair(wn + 2 * C::W_TILE + row * 128, wn + row * 128, row, i0, i1);  // W_i, -W_i
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&full_bar[stage]);
+          mbar_arrive(&pempty[ps]);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++ps == P_STAGES) { ps = 0; pph ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ TMA producer of packed words
+    if (lane == 0) {
+      int ps = 0;
+      uint32_t pph = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int b, nt, mt;
+        swap_coords(t, tiles_m, tiles_n, b, nt, mt);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&pempty[ps], pph ^ 1);
+          uint8_t* dst = packed + ps * C::P_STAGE_BYTES;
+          mbar_arrive_expect_tx(&pfull[ps], C::P_STAGE_BYTES);
+          tma_load_3d(dst, &tmX, &pfull[ps], kb * KBW, nt * TN, 2 * b);
+          tma_load_3d(dst + C::P_PLANE_X, &tmX, &pfull[ps], kb * KBW, nt * TN, 2 * b + 1);
+          tma_load_3d(dst + 2 * C::P_PLANE_X, &tmW, &pfull[ps], kb * KBW, mt * TM, 2 * b);
+          tma_load_3d(dst + 2 * C::P_PLANE_X + C::P_PLANE_W, &tmW, &pfull[ps], kb * KBW, mt * TM, 2 * b + 1);
+          if (++ps == P_STAGES) { ps = 0; pph ^= 1; }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int TM, bool TMA_STORE>
+cudaError_t launch_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC, const GemmB1Args& a,
+                        int num_sms, cudaStream_t stream) {
+  using C = SwapCfg<TM>;
+  auto kern = cgemm_b1_f4_swap_kernel<TM, TMA_STORE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = (a.M + TM - 1) / TM, tiles_n = (a.N + TN - 1) / TN;
+  const long long nt = (long long)tiles_m * tiles_n * a.B;
+  if (nt > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int grid = (int)(nt < num_sms ? nt : num_sms);
+  kern<<<grid, C::NUM_THREADS, C::SMEM_BYTES, stream>>>(tmW, tmX, tmC, a, tiles_m, tiles_n, (int)nt);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int gemm_b1_f4_swap_beams(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 0); }
+
+cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
+                                   const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream) {
+  if (gemm_b1_f4_swap_beams(args.M) == 32)
+    return tma_store ? launch_swap<32, true>(tmW, tmX, tmC, args, num_sms, stream)
+                     : launch_swap<32, false>(tmW, tmX, tmC, args, num_sms, stream);
+  return tma_store ? launch_swap<64, true>(tmW, tmX, tmC, args, num_sms, stream)
+                   : launch_swap<64, false>(tmW, tmX, tmC, args, num_sms, stream);
+}
+
+}  // namespace tcbf

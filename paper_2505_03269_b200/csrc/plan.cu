@@ -216,6 +216,10 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
     if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
     if (plan->b1_tc == 3) return plan->N % 4 ? "b1_tcgen05_i8_2cta_256x128_stg" : "b1_tcgen05_i8_2cta_256x128_tma";
+    if (plan->b1_tc == 4 && tcbf::gemm_b1_f4_swap_beams(plan->M) && !getenv("TCBF_NO_SWAP"))
+      return tcbf::gemm_b1_f4_swap_beams(plan->M) == 32
+                 ? (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x32_stg" : "b1_tcgen05_mxf4pm1_swap_128x32_tma")
+                 : (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x64_stg" : "b1_tcgen05_mxf4pm1_swap_128x64_tma");
     if (plan->b1_tc == 4) return plan->N % 4 ? "b1_tcgen05_mxf4pm1_128x128_stg" : "b1_tcgen05_mxf4pm1_128x128_tma";
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
@@ -368,7 +372,24 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
         const int64_t bpr = 256 * plan->kp * 8;
         a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bpr, (plan->M + 255) / 256));
       }
-      if (plan->b1_tc == 4) {  // packed words by TMA: box {one 256-bit K block, 128 rows}
+      const int swap_tm = plan->b1_tc == 4 && getenv("TCBF_NO_SWAP") == nullptr
+                              ? tcbf::gemm_b1_f4_swap_beams(plan->M) : 0;
+      if (swap_tm) {  // few beams: samples on the 128-row MMA dimension, beams on N
+        CUtensorMap tw, tx;
+        const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
+        s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw,
+                      (uint32_t)swap_tm, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+        if (s != TCBF_OK) return s;
+        s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+        if (s != TCBF_OK) return s;
+        if (tma_store) {  // 32 beams x 32 samples boxes, unswizzled 128-byte rows
+          s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+          if (s != TCBF_OK) return s;
+        }
+        e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, tma_store, plan->num_sms, st);
+      } else if (plan->b1_tc == 4) {  // packed words by TMA: box {one 256-bit K block, 128 rows}
         CUtensorMap tw, tx;
         if (tma_store && tcbf::gemm_b1_f4_store_box_cols(plan->kp) == 16) {  // 32 x 16 boxes, 64-byte swizzle
           s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 16, 32,

@@ -481,6 +481,33 @@ def test_b1_random_corpus(tcbf, b1_kernel):
         assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, M, N, K, 1)), (M, N, K)
 
 
+@pytest.mark.parametrize("shape", [(32, 512, 4096 + 5, 1), (64, 1000, 3000, 1), (17, 260, 700, 2), (48, 77, 600, 2),
+                                   (1, 128, 256, 3), (33, 4096, 1024, 1)])
+def test_b1_small_m_swapped_kernel_bit_exact(tcbf, shape):
+    """Few-beam plans (M <= 64) run the swapped fp4 kernel (samples on the 128-row MMA dimension):
+    ragged M/N/K, N % 4 != 0 (masked stores), both beam-tile widths."""
+    M, N, K, B = shape
+    w = synth.generate("adc", 41, 0, B, M, K)
+    x = synth.generate("adc", 41, 1, B, K, N)
+    plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    assert "swap" in plan.variant
+    assert np.array_equal(y, oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B))
+
+
+def test_full_size_m32_b1_16384(tcbf):
+    """BASELINE configs[4] small-beam 1-bit point M=32, N=K=16384 at full size, whole output."""
+    M = 32
+    N = K = 16384
+    seed = synth.SEED_BASE + 4
+    plan = tcbf.Plan(M, N, K, 1, "b1")
+    wd = synth.generate_device("uniform", seed, 0, 1, M, K)
+    xd = synth.generate_device("uniform", seed, 1, 1, K, N)
+    y = plan.beamform(plan.pack(tcbf.WEIGHTS, wd), plan.pack(tcbf.DATA, xd)).cpu().numpy()
+    assert "swap" in plan.variant
+    ref = oracle.cgemm_b1(wd.cpu().numpy(), xd.cpu().numpy(), 0, M, N, K, 1)
+    assert np.array_equal(y, ref)
+
+
 @pytest.mark.parametrize("splits", ["auto", "3", "7"])
 def test_b1_split_k_bit_exact(tcbf, monkeypatch, splits):
     """Split-K (int8 kernel, TMA reduce-add of exact int32 partials): the M=32 sweep shape class
