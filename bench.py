@@ -312,19 +312,19 @@ def pack_weights(plan, c, seed, dev, b0, max_src_bytes=8 << 30):
     if B * M * K * 8 <= max_src_bytes:
         wsrc = synth.generate_device(c["wd"], seed, 0, B, M, K, device=dev, b0=b0)
         return plan.pack(tcbf.WEIGHTS, wsrc)
-    assert B == 1, "row-sliced weight generation implemented for batch 1"
     wp = plan.alloc_packed(tcbf.WEIGHTS, dev)
     rows = max(1, max_src_bytes // (K * 8))
-    for m0 in range(0, M, rows):
-        mr = min(rows, M - m0)
-        sub = tcbf.Plan(mr, c["N"], K, 1, c["prec"])
-        # rows m0..m0+mr of entry b0 of the global [*, M, K] weight tensor: element offset (b0*M + m0)*K
-        src = synth.generate_device(c["wd"], seed, 0, 1, mr, K, device=dev, b0=0,
-                                    offset_elems=(b0 * M + m0) * K)
-        part = sub.pack(tcbf.WEIGHTS, src)
-        del src
-        wp[0, :, m0:m0 + mr].copy_(part[0])
-        del part
+    for b in range(B):
+        for m0 in range(0, M, rows):
+            mr = min(rows, M - m0)
+            sub = tcbf.Plan(mr, c["N"], K, 1, c["prec"])
+            # rows m0..m0+mr of entry b0+b of the global [*, M, K] weight tensor
+            src = synth.generate_device(c["wd"], seed, 0, 1, mr, K, device=dev, b0=0,
+                                        offset_elems=((b0 + b) * M + m0) * K)
+            part = sub.pack(tcbf.WEIGHTS, src)
+            del src
+            wp[b, :, m0:m0 + mr].copy_(part[0])
+            del part
     torch.cuda.synchronize()
     return wp
 

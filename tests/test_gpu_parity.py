@@ -579,12 +579,13 @@ def test_sliced_weight_generation_equals_direct(tcbf):
     """bench.pack_weights' row-sliced generate+pack (for model matrices too large for one fp32
     source) produces exactly the directly packed weights."""
     import bench
-    c = dict(bench.CONFIGS["ultrasound_b1_planes"], M=1000, K=3000, N=64)
-    seed = synth.SEED_BASE + 3
-    plan = tcbf.Plan(c["M"], c["N"], c["K"], 1, "b1")
-    direct = plan.pack(tcbf.WEIGHTS, synth.generate_device(c["wd"], seed, 0, 1, c["M"], c["K"]))
-    sliced = bench.pack_weights(plan, c, seed, torch.device("cuda"), 0, max_src_bytes=300 * 3000 * 8)
-    assert torch.equal(direct, sliced)
+    for prec, B, b0 in [("b1", 1, 0), ("b1", 3, 2), ("f16", 2, 1)]:
+        c = dict(bench.CONFIGS["ultrasound_b1_planes"], M=1000, K=3000, N=64, B=B, prec=prec)
+        seed = synth.SEED_BASE + 3
+        plan = tcbf.Plan(c["M"], c["N"], c["K"], B, prec)
+        direct = plan.pack(tcbf.WEIGHTS, synth.generate_device(c["wd"], seed, 0, B, c["M"], c["K"], b0=b0))
+        sliced = bench.pack_weights(plan, c, seed, torch.device("cuda"), b0, max_src_bytes=300 * 3000 * 8)
+        assert torch.equal(direct, sliced), (prec, B, b0)
 
 
 def test_full_size_ultrasound_b1_planes_sampled(tcbf):
