@@ -429,13 +429,7 @@ def run_tcbf(args, c):
     peaks = load_peaks()
     roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
                         fused=fused)
-    if not fused:
-        roof["kernel"] = plan.variant
-    elif c["prec"] == "b1":
-        roof["kernel"] = "b1_tcgen05_i8_fused_pack_128x128"
-    else:
-        roof["kernel"] = ("f16_tcgen05_fused_pack_bres_128x128" if plan.k_packed <= 256 else
-                          "f16_tcgen05_stream_conv_128x128")
+    roof["kernel"] = plan.raw_variant if fused else plan.variant
     roof["traffic"] = traffic_for(args.config, roof["kernel"])
     roof["kernel_ms"] = round(gemm_ms_max, 4)
     roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)

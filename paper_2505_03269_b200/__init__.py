@@ -200,6 +200,20 @@ class Plan:
         units = tiles * _conv_splits(tiles, (self.K + 31) // 32, _num_sms())
         return self.M <= 128 and (units >= _num_sms() // 4 or "TCBF_FORCE_STREAM_CONV" in os.environ)
 
+    @property
+    def raw_variant(self) -> str:
+        """Kernel that beamform_raw launches for this plan (mirror of the dispatch in plan.cu)."""
+        if not self.raw_fused:
+            return self.variant
+        if self.precision == B1:
+            return "b1_tcgen05_i8_fused_pack_128x128"
+        if self.k_packed <= 256:
+            units = (self.N + 127) // 128 * self.batch
+            if self.M >= 256 and units >= 2 and os.environ.get("TCBF_F16_FUSED") == "2":
+                return "f16_tcgen05_fused_pack_bres_2cta_256x128"
+            return "f16_tcgen05_fused_pack_bres_128x128"
+        return "f16_tcgen05_stream_conv_128x128"
+
     def steering_weights(self, positions, angles, freqs, c, layout="interleaved", out=None, stream=None):
         """fp32 weight source w[b][m][k] = exp(+2 pi i f_b d_k sin(theta_m) / c).
         positions [K], angles [M], freqs [B]: cuda float64 tensors."""

@@ -65,6 +65,18 @@ __device__ __forceinline__ uint64_t desc_b_res(const void* plane, uint32_t k_row
   return d;
 }
 
+// timeline stamps (dev only): per CTA 1024 slots; tile it: [4*it + 0..3] = MMA start / MMA issued /
+// epilogue got tile / epilogue done; unit ui: [512 + 4*ui + 0..3] = MMA waits B0 / got B0 /
+// converters got bempty0 / converted block 0
+constexpr int TRACE_SLOTS = 1024;
+__device__ __forceinline__ void stamp(unsigned long long* tr, int slot) {
+  if (tr && slot < TRACE_SLOTS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * TRACE_SLOTS + slot] = t;
+  }
+}
+
 __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -130,9 +142,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&aempty[stage], phase ^ 1);
             uint8_t* st = sA + stage * A_STAGE_BYTES;
-            mbar_arrive_expect_tx(&afull[stage], A_STAGE_BYTES);
-            tma_load_3d(st, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b);
-            tma_load_3d(st + A_BYTES, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b + 1);
+            if ((args.debug & 4) && mt > 0) {  // ablation: weight tiles loaded once per unit (wrong values)
+              mbar_arrive(&afull[stage]);
+            } else {
+              mbar_arrive_expect_tx(&afull[stage], A_STAGE_BYTES);
+              tma_load_3d(st, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b);
+              tma_load_3d(st + A_BYTES, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b + 1);
+            }
             if (++stage == A_STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -152,10 +168,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int abuf = it & 1;
           mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
+          stamp(args.trace, 4 * it);
           const uint32_t d_re = tmem_base + abuf * 2 * BN;
           const uint32_t d_im = d_re + BN;
           for (int kb = 0; kb < num_kb; ++kb) {
+            if (mt == 0 && kb == 0) stamp(args.trace, 512 + 4 * ui);
             if (mt == 0) mbar_wait(&bfull[kb], bphase);  // resident B block converted
+            if (mt == 0 && kb == 0) stamp(args.trace, 512 + 4 * ui + 1);
             mbar_wait(&afull[stage], phase);
             tc_fence_after();
             uint8_t* st = sA + stage * A_STAGE_BYTES;
@@ -165,6 +184,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t ar = desc_a128(st, kk * 32), ai = desc_a128(st + A_BYTES, kk * 32);
               const uint64_t br = desc_b_res(sB, krow), bi = desc_b_res(sB + B_PLANE_BYTES, krow);
               const uint32_t acc = (kb | kk) ? 1u : 0u;
+              if (args.debug & 2) continue;
               mma_f16_ss(d_re, ar, br, IDESC, acc);
               mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);
               mma_f16_ss(d_im, ar, bi, IDESC, acc);
@@ -175,6 +195,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++stage == A_STAGES) { stage = 0; phase ^= 1; }
           }
           mma_commit(&tfull[abuf]);
+          stamp(args.trace, 4 * it + 1);
         }
       }
     }
@@ -192,6 +213,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int abuf = it & 1;
         mbar_wait(&tfull[abuf], (it >> 1) & 1);
         tc_fence_after();
+        if (threadIdx.x == 64) stamp(args.trace, 4 * it + 2);
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BN;
         uint32_t v[2][32];
         tmem_ld_32x32b_x32(tbase, v[0]);
@@ -208,6 +230,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) mbar_arrive(&tempty[abuf]);
           }
           const uint32_t* vv = v[ch & 1];
+          if (args.debug & 1) continue;
+          if (args.debug & 16) {  // experiment: direct 256-bit stores from registers (no smem staging)
+            const int m = m0 + q * 32 + lane;
+            const int nb = n0 + c * 32;
+            if (m < args.M && nb + 32 <= args.N) {
+              float* row = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
+#pragma unroll
+              for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
+            }
+            continue;
+          }
           // cooperative staging: the 4 epilogue warps fill one 128-row x 32-column box (16 KB),
           // one thread issues a single TMA store per chunk
           uint8_t* buf = epi_base + sbuf * 16384;
@@ -228,6 +261,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           sbuf ^= 1;
         }
+        if (threadIdx.x == 64) stamp(args.trace, 4 * it + 3);
       }
     }
     if (threadIdx.x == 64) bulk_wait_group<0>();
@@ -273,6 +307,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
         }
+        if (ct == 0 && kb == 0) stamp(args.trace, 512 + 4 * ui + 2);
         mbar_wait(&bempty[kb], (ui & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -288,6 +323,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bfull[kb]);
+        if (ct == 0 && kb == 0) stamp(args.trace, 512 + 4 * ui + 3);
       }
     }
   }

@@ -14,6 +14,7 @@ struct GemmF16Args {
   int debug;   // ablation (TCBF_DEBUG): bit0 skip output stores, bit1 skip MMAs
   int group_m; // tile rows per rasterisation group (tile_coords)
   int splits, kb_per_split;  // K split of the streaming-conversion kernel (fp32 TMA reduce-add)
+  unsigned long long* trace;  // dev timeline (TCBF_TRACE=<file>, fused kernel): globaltimer stamps
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
@@ -45,6 +46,8 @@ int gemm_f16_conv_block_k();
 int gemm_f16_conv_splits(int tiles, int num_kb, int num_sms);
 cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                  const GemmF16Args& args, int layout, int num_sms, cudaStream_t stream);
+cudaError_t launch_gemm_f16_fused2(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
+                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 

@@ -452,7 +452,35 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     if (nu > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
     a.num_tiles = (int)(nu * a.tiles_m);
     a.out = static_cast<float*>(out);
-    cudaError_t e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
+    const char* trace_file = getenv("TCBF_TRACE");  // dev timeline of the fused kernel
+    if (trace_file) {
+      cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
+      cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
+    }
+    // CTA-pair variant (M=256 MMAs, data half resident per CTA, double-buffered): bit-identical
+    // but measured no faster on radio (665 vs 643 us: the tile loop is bound by the tensor rate
+    // and the HBM stores under one power budget, not by shared memory), so it is opt-in
+    // (TCBF_F16_FUSED=2)
+    const bool pair = plan->M >= 256 && nu >= 2 && getenv("TCBF_F16_FUSED") && atoi(getenv("TCBF_F16_FUSED")) == 2;
+    cudaError_t e;
+    if (pair) {
+      a.tiles_m = (int)((plan->M + 255) / 256);
+      a.num_tiles = (int)(nu * a.tiles_m);
+      e = tcbf::launch_gemm_f16_fused2(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    } else {
+      e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
+    }
+    if (trace_file) {
+      std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
+      cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(a.trace);
+      if (FILE* f = fopen(trace_file, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
     if (e != cudaSuccess) return cuda_fail(e, "fused beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;

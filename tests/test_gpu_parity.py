@@ -209,6 +209,8 @@ def test_inputs_unmodified(tcbf):
 RAW_SHAPES = [
     (200, 300, 100, 3, "interleaved"),   # fused, ragged M/N/K, N % 8 != 0 -> scalar loads
     (256, 256, 256, 2, "interleaved"),   # fused, vector loads, exactly K16 = 256
+    (600, 300, 200, 3, "planar"),        # fused (pair: 3 pair tiles, ragged M and N), planar
+    (512, 1000, 256, 2, "interleaved"),  # fused (pair: 16 units on 8 pairs -> both B buffers)
     (130, 136, 64, 3, "planar"),         # fused, planar source
     (8, 64, 32, 2, "interleaved"),       # tiny (BASELINE configs[0])
     (64, 96, 300, 2, "interleaved"),     # K16 = 320 > 256, M <= 128 -> streaming-conversion kernel
@@ -219,10 +221,12 @@ RAW_SHAPES = [
 ]
 
 
-@pytest.fixture(params=["auto", "force_stream"])
+@pytest.fixture(params=["auto", "force_stream", "pair"])
 def raw_mode(request, monkeypatch):
     if request.param == "force_stream":   # small-M shapes through the streaming-conversion kernel
         monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
+    if request.param == "pair":           # short-K shapes with M >= 256 through the CTA-pair fused kernel
+        monkeypatch.setenv("TCBF_F16_FUSED", "2")
     return request.param
 
 
