@@ -50,6 +50,11 @@ CONFIGS = {
     # K = 128 frequencies x 64 transceivers x 32 transmissions, a block of 1024 frames per step
     "ultrasound_b1_planes": _cfg("b1", 3 * 128 * 128, 1024, 128 * 64 * 32, 1, "phase_amp", "adc_scaled", 3,
                                  "ultrasound 1-bit: M=49152 voxels (3 planes), K=262144, N=1024 frames"),
+    # NEXT-1: the radio shape with the data already fp16 interleaved (an fp16 producer,
+    # PAPER.md:103), beamformed with no data pack by tcbf_beamform_f16i
+    "radio_f16i": dict(_cfg("f16", 1024, 1024, 256, 256, "phase", "adc", 1,
+                            "radio fp16, data delivered as interleaved fp16 (no pack): M=1024, K=256, N=1024, "
+                            "batch=256"), src="f16i"),
     # Fig. 3 extra rows
     "fig3_f16_small": _cfg("f16", 1024, 1024, 64, 256, "uniform", "uniform", 4, "fp16 small 256x1024x1024x64"),
     "fig3_b1_small": _cfg("b1", 1024, 1024, 256, 256, "uniform", "uniform", 4, "int1 small 256x1024x1024x256"),
@@ -356,6 +361,9 @@ def run_tcbf(args, c):
 
     wp = pack_weights(plan, c, seed, dev, sh.b0)
     xsrc = synth.generate_device(c["xd"], seed, 1, B, K, N, device=dev, b0=sh.b0)
+    f16i = c.get("src") == "f16i"
+    if f16i:   # the producer delivers interleaved fp16 (conversion outside the timed region)
+        xsrc = xsrc.half()
     xp = plan.alloc_packed(tcbf.DATA, dev)
     out = plan.alloc_output(dev)
     torch.cuda.synchronize()
@@ -366,7 +374,9 @@ def run_tcbf(args, c):
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        if plan.raw_fused:
+        if f16i:
+            plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
+        elif plan.raw_fused:
             plan.beamform_raw(wp, xsrc, out=out, stream=stream)
         else:
             plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
@@ -377,6 +387,8 @@ def run_tcbf(args, c):
             flush_buf.fill_(1.0)
         step()
     torch.cuda.synchronize()
+    # kernels per step, as the library counts them (pack: 1; beamform: 1, or memset + kernel on split K)
+    launches_per_step = tcbf.Plan.last_launch_count() + (0 if (f16i or plan.raw_fused) else 1)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     sampler = ClockSampler(local)
@@ -384,12 +396,15 @@ def run_tcbf(args, c):
         dist.barrier()
     torch.cuda.synchronize()
     sampler.start()
-    fused = plan.raw_fused
+    fused = plan.raw_fused and not f16i
     for i in range(args.steps):
         if flush:
             flush_buf.fill_(float(i))   # evict L2 between timed steps (not inside the timed spans)
         ev[i][0].record(stream)
-        if fused:
+        if f16i:
+            ev[i][1].record(stream)
+            plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
+        elif fused:
             ev[i][1].record(stream)
             plan.beamform_raw(wp, xsrc, out=out, stream=stream)
         else:
@@ -416,12 +431,22 @@ def run_tcbf(args, c):
     x_host = xsrc.cpu().pin_memory()
     out_host = torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory()
     e2e_steps = max(1, min(args.steps, int(os.environ.get("TCBF_E2E_STEPS", "5"))))
-    plan.beamform_host(wp, x_host, out_host)
+
+    def e2e_call():
+        if f16i:   # H2D of the fp16 data, beamform_f16i, D2H of the output (binding-level API)
+            xsrc.copy_(x_host, non_blocking=True)
+            plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
+            out_host.copy_(out, non_blocking=True)
+            torch.cuda.synchronize()
+        else:
+            plan.beamform_host(wp, x_host, out_host)
+
+    e2e_call()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        plan.beamform_host(wp, x_host, out_host)
+        e2e_call()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     e2e_s = max_over_ranks(e2e_s, dev)
     e2e_val = world * useful_ops(c) / e2e_s / 1e12
@@ -429,7 +454,7 @@ def run_tcbf(args, c):
     peaks = load_peaks()
     roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
                         fused=fused)
-    roof["kernel"] = plan.raw_variant if fused else plan.variant
+    roof["kernel"] = "f16_tcgen05_interleaved_128x64" if f16i else (plan.raw_variant if fused else plan.variant)
     roof["traffic"] = traffic_for(args.config, roof["kernel"])
     roof["kernel_ms"] = round(gemm_ms_max, 4)
     roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
@@ -442,7 +467,8 @@ def run_tcbf(args, c):
         "vs_baseline": None, "dtype": c["prec"], "data": "synthetic (seeded counter-based generator, synth/)",
         "config": {"workload": args.config, "desc": c["desc"], "M": M, "N": N, "K": K, "batch_per_gpu": B,
                    "global_batch": B * world, "precision": c["prec"],
-                   "step": ("tcbf_beamform_raw (data pack fused into the GEMM)" if fused else
+                   "step": ("tcbf_beamform_f16i (fp16 interleaved data, no pack)" if f16i else
+                            "tcbf_beamform_raw (data pack fused into the GEMM)" if fused else
                             "tcbf_pack(data) + tcbf_beamform") + "; weights packed once",
                    "l2": ("flushed between steps (256 MiB write)" if flush else
                           f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
@@ -450,10 +476,13 @@ def run_tcbf(args, c):
                    "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4),
                    "samples_per_s": round(frames_per_s, 1)},
         "roofline": roof,
-        "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s", "h2d_bytes_per_step": int(x_host.numel() * 4),
-                "d2h_bytes_per_step": int(plan.out_bytes), "api": "tcbf_beamform_host (pinned host buffers)",
+        "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s",
+                "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
+                "d2h_bytes_per_step": int(plan.out_bytes),
+                "api": ("Plan.beamform_f16i with pinned-host copies in and out" if f16i else
+                        "tcbf_beamform_host (pinned host buffers)"),
                 "steps": e2e_steps},
-        "gpu_launches": (1 if fused else 2) * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": sampler.summary(),
     }
     j = sampler.joules()

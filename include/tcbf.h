@@ -120,6 +120,22 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
 tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
                               tcbf_src_layout layout, void* out, void* stream);
 
+/* 16-bit-mode beamforming on data that is already fp16 and INTERLEAVED complex -- the natural
+ * format of fp16 producers, with no data pack at all (the paper's future-work
+ * kernel "that does not require this transpose").
+ *   plan      F16 plan (INVALID_ARG otherwise); N % 4 == 0 (16-byte data / output row strides).
+ *   w_packed  packed weights from tcbf_pack(plan, TCBF_WEIGHTS, ...), device.
+ *   x_f16     device, caller-owned, read-only: [B][K][N] complex as interleaved IEEE binary16
+ *             pairs (re, im) -- 4 bytes per sample, N contiguous, 16-byte aligned.
+ *   out       device [B][2][M][N] fp32 (plane 0 = Re, 1 = Im), 16-byte aligned.
+ * The data is read as a real K x 2N matrix: two real GEMMs per K step (A_r X, A_i X) and the
+ * epilogue recombines Re = (A_r X)[2n] - (A_i X)[2n+1], Im = (A_r X)[2n+1] + (A_i X)[2n].  Same
+ * exact fp16 products and fp32 accumulation as tcbf_beamform; the final combination of the two
+ * accumulators is one more fp32 rounding (within the 16-bit tolerance, not bit-identical).
+ * Asynchronous on `stream`; one kernel launch. */
+tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, const void* x_f16, void* out,
+                               void* stream);
+
 /* Steering weights for a far-field plane wave (Eqs. 1-3): writes the plan's fp32
  * weight source (interleaved [B][M][K] float2 or planar [B][2][M][K], per `layout`) with
  *     w[b][m][k] = exp(+2 pi i freqs[b] positions[k] sin(angles[m]) / c)

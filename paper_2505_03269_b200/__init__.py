@@ -63,6 +63,8 @@ def lib():
         L.tcbf_beamform.argtypes = [vp, vp, vp, vp, vp]
         L.tcbf_beamform_raw.restype = ctypes.c_int
         L.tcbf_beamform_raw.argtypes = [vp, vp, vp, ctypes.c_int, vp, vp]
+        L.tcbf_beamform_f16i.restype = ctypes.c_int
+        L.tcbf_beamform_f16i.argtypes = [vp, vp, vp, vp, vp]
         L.tcbf_steering_weights.restype = ctypes.c_int
         L.tcbf_steering_weights.argtypes = [vp, vp, vp, vp, ctypes.c_double, ctypes.c_int, vp, vp]
         L.tcbf_beamform_host.restype = ctypes.c_int
@@ -184,6 +186,16 @@ class Plan:
                                        ctypes.c_void_p(x_src.data_ptr()), _LAYOUT[layout],
                                        ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream, w_packed.device)),
                "tcbf_beamform_raw")
+        return out
+
+    def beamform_f16i(self, w_packed, x_f16, out=None, stream=None):
+        """16-bit beamform of fp16 interleaved complex data x_f16 [B][K][N][2] (torch.float16, cuda),
+        no data pack (NEXT-1)."""
+        if out is None:
+            out = self.alloc_output(w_packed.device)
+        _check(lib().tcbf_beamform_f16i(self._h, ctypes.c_void_p(w_packed.data_ptr()),
+                                        ctypes.c_void_p(x_f16.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                        _stream_ptr(stream, w_packed.device)), "tcbf_beamform_f16i")
         return out
 
     @property

@@ -42,6 +42,10 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
                             cudaStream_t stream);
 
 bool gemm_f16_fused_supported(int64_t K16, int64_t N);
+int gemm_f16_ileave_block_k();
+int gemm_f16_ileave_block_n();
+cudaError_t launch_gemm_f16_ileave(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
+                                   const GemmF16Args& args, int num_sms, cudaStream_t stream);
 int gemm_f16_conv_block_k();
 int gemm_f16_conv_splits(int tiles, int num_kb, int num_sms);
 cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,

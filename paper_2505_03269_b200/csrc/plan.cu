@@ -575,6 +575,48 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   return s;
 }
 
+tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, const void* x_f16, void* out,
+                               void* stream) {
+  g_launches = 0;
+  if (!plan || !w_packed || !x_f16 || !out) return fail(TCBF_ERR_INVALID_ARG, "NULL argument");
+  if (plan->prec != TCBF_PREC_F16) return fail(TCBF_ERR_INVALID_ARG, "tcbf_beamform_f16i needs an F16 plan");
+  if (plan->N % 4) return fail(TCBF_ERR_INVALID_ARG, "tcbf_beamform_f16i needs N %% 4 == 0");
+  if (!aligned(w_packed, 16) || !aligned(x_f16, 16) || !aligned(out, 16))
+    return fail(TCBF_ERR_INVALID_ARG, "operands and output must be 16-byte aligned");
+  tcbf_status s = check_device(plan);
+  if (s != TCBF_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int bk = tcbf::gemm_f16_ileave_block_k(), bnc = tcbf::gemm_f16_ileave_block_n();
+  CUtensorMap ta, tx, tc;
+  s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (s != TCBF_OK) return s;
+  // interleaved data as a real [B][K][2N] fp16 matrix: 64-column x BK-row MN-major boxes
+  s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_f16, 2 * plan->N, plan->K, plan->B, 64, bk,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (s != TCBF_OK) return s;
+  s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+  if (s != TCBF_OK) return s;
+  tcbf::GemmF16Args a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+  a.tiles_m = (int)((plan->M + 127) / 128);
+  a.tiles_n = (int)((plan->N + bnc - 1) / bnc);
+  const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
+  if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+  a.num_tiles = (int)nt;
+  a.num_kb = (int)(plan->kp / bk);
+  {  // rasterisation group: ~48 MB of weight rows in L2
+    const int64_t bytes_per_tile_row = 128 * plan->kp * 4;
+    a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((48ll << 20) / bytes_per_tile_row, a.tiles_m));
+  }
+  cudaError_t e = tcbf::launch_gemm_f16_ileave(ta, tx, tc, a, plan->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "interleaved-fp16 beamform kernel launch");
+  g_launches = 1;
+  return TCBF_OK;
+}
+
 tcbf_status tcbf_steering_weights(const tcbf_plan* plan, const double* positions, const double* angles,
                                   const double* freqs, double c, tcbf_src_layout layout, float* dst,
                                   void* stream) {

@@ -277,6 +277,51 @@ def test_f16_beamform_raw_split_k(tcbf, shape, splits, monkeypatch):
     _check_f16(y_raw.cpu().numpy(), ref, w, x)
 
 
+# ------------------------------------------------------------------ fp16 interleaved data, no pack (NEXT-1)
+@pytest.mark.parametrize("shape", [(8, 64, 32, 2), (200, 300, 100, 3), (130, 136, 64, 3), (300, 1000, 480, 2),
+                                   (1024, 1024, 256, 2), (1000, 260, 333, 1), (64, 4, 16, 1)])
+def test_f16i_interleaved_fp16_beamform(tcbf, shape):
+    """tcbf_beamform_f16i on fp16 interleaved data (read as a real K x 2N matrix, Re/Im recombined
+    in the epilogue): within the 16-bit tolerance of the oracle on the same fp16 values, and equal
+    to the planar path up to one fp32 rounding."""
+    M, N, K, B = shape
+    w = synth.generate("phase", 29, 0, B, M, K)
+    x = synth.generate("adc", 29, 1, B, K, N)
+    wi, xi = synth.to_interleaved(w), synth.to_interleaved(x)
+    x16 = xi.astype(np.float16)  # numpy RNE: the same fp16 values the oracle rounds to
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(wi))
+    y = plan.beamform_f16i(wp, torch.from_numpy(x16).cuda())
+    assert tcbf.Plan.last_launch_count() == 1
+    y_planar = plan.beamform(wp, plan.pack(tcbf.DATA, _dev(xi)))
+    torch.cuda.synchronize()
+    scale = y_planar.abs().max().item()
+    assert (y - y_planar).abs().max().item() <= 1e-5 * scale
+    _check_f16(y.cpu().numpy(), oracle.cgemm_f16(wi, xi, 0, M, N, K, B), w, x)
+
+
+def test_f16i_integer_inputs_exact(tcbf):
+    """Integer-valued fp16 inputs with small partial sums: every product and sum is exact, so the
+    interleaved path equals the oracle exactly (SURVEY §8(c) pin iv)."""
+    M, N, K, B = 96, 200, 130, 2
+    rng = np.random.default_rng(5)
+    w = (rng.integers(-2, 3, (B, M, K, 2))).astype(np.float32)
+    x = (rng.integers(-2, 3, (B, K, N, 2))).astype(np.float32)
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    y = plan.beamform_f16i(plan.pack(tcbf.WEIGHTS, _dev(w)), torch.from_numpy(x.astype(np.float16)).cuda())
+    assert np.array_equal(y.cpu().numpy().astype(np.float64), oracle.cgemm_f16(w, x, 0, M, N, K, B))
+
+
+def test_f16i_errors(tcbf):
+    plan = tcbf.Plan(8, 6, 8, 1, "f16")   # N % 4 != 0
+    wp = plan.alloc_packed(tcbf.WEIGHTS)
+    with pytest.raises(tcbf.TcbfError):
+        plan.beamform_f16i(wp, torch.zeros(1, 8, 6, 2, dtype=torch.float16, device="cuda"))
+    pb = tcbf.Plan(8, 8, 8, 1, "b1")
+    with pytest.raises(tcbf.TcbfError):
+        pb.beamform_f16i(pb.alloc_packed(tcbf.WEIGHTS), torch.zeros(1, 8, 8, 2, dtype=torch.float16, device="cuda"))
+
+
 @pytest.mark.parametrize("shape", [(70, 44, 300, 2), (200, 260, 512, 3), (8, 64, 32, 2), (130, 132, 33, 2),
                                    (300, 1000, 480, 1)])
 @pytest.mark.parametrize("layout", ["interleaved", "planar"])
