@@ -16,6 +16,7 @@
 //
 // Bit-identical to tcbf_pack(DATA) + tcbf_beamform (same rounding, same MMA order).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -82,7 +83,35 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int LAYOUT, bool VEC>
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA load multicast to both CTAs of the pair (same smem offset, each CTA's own barrier)
+__device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, int32_t c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// MC: CTA pairs (clusters of 2) take adjacent units of the same batch entry, so their weight
+// tiles are identical: each CTA TMA-loads one of the two weight planes and multicasts it to both
+// (half the L2 -> SM weight traffic); both MMA issuers release a stage in both CTAs.
+template <int LAYOUT, bool VEC, bool MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cgemm_f16_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                            GemmF16Args args, const float* __restrict__ xsrc, int K) {
@@ -104,11 +133,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_kb = args.num_kb;  // K16 / 64 <= 4
   const int tiles_m = args.tiles_m, tiles_n = args.tiles_n;
   const int num_units = args.B * tiles_n;
+  // unit walk: single CTAs stride over all units; pairs take units (2p + rank) (tiles_n even)
+  const int rank = MC ? (int)cluster_ctarank() : 0;
+  const int u_first = MC ? 2 * (int)(blockIdx.x >> 1) + rank : (int)blockIdx.x;
+  const int u_step = MC ? 2 * (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < A_STAGES; ++s) {
       mbar_init(&afull[s], 1);
-      mbar_init(&aempty[s], 1);
+      mbar_init(&aempty[s], MC ? 2 : 1);
     }
     for (int s = 0; s < KMAX / BK; ++s) {
       mbar_init(&bfull[s], CONV_WARPS);
@@ -127,7 +160,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_relinquish();
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // peers signal this CTA's barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -136,7 +169,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         for (int mt = 0; mt < tiles_m; ++mt) {
           for (int kb = 0; kb < num_kb; ++kb) {
@@ -146,8 +179,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_arrive(&afull[stage]);
             } else {
               mbar_arrive_expect_tx(&afull[stage], A_STAGE_BYTES);
-              tma_load_3d(st, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b);
-              tma_load_3d(st + A_BYTES, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b + 1);
+              if (MC) {
+                tma_load_3d_mc(st + rank * A_BYTES, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b + rank);
+              } else {
+                tma_load_3d(st, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b);
+                tma_load_3d(st + A_BYTES, &tmA, &afull[stage], kb * BK, mt * BM, 2 * b + 1);
+              }
             }
             if (++stage == A_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -190,7 +227,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mma_f16_ss(d_im, ar, bi, IDESC, acc);
               mma_f16_ss(d_im, ai, br, IDESC, 1u);
             }
-            mma_commit(&aempty[stage]);
+            if (MC) mma_commit_mc(&aempty[stage]);  // the stage is free in both CTAs
+            else mma_commit(&aempty[stage]);
             if (mt == tiles_m - 1) mma_commit(&bempty[kb]);  // last reader of this B block
             if (++stage == A_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -205,7 +243,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr int CHUNKS = BN / 32;
     int sbuf = 0;
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = u_first; u < num_units; u += u_step) {
       const int b = u / tiles_n;
       const int n0 = (u - b * tiles_n) * BN;
       for (int mt = 0; mt < tiles_m; ++mt, ++it) {
@@ -329,23 +367,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // no CTA exits while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
 }
 
-template <int LAYOUT, bool VEC>
+template <int LAYOUT, bool VEC, bool MC>
 cudaError_t launch_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& a, const float* x,
                          int K, int num_sms, cudaStream_t s) {
-  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC>;
+  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = a.B * a.tiles_n;
-  const int grid = units < num_sms ? units : num_sms;
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(tmA, tmC, a, x, K);
+  if (!MC) {
+    const int grid = units < num_sms ? units : num_sms;
+    kern<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(tmA, tmC, a, x, K);
+    return cudaGetLastError();
+  }
+  const int pairs = units / 2 < num_sms / 2 ? units / 2 : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmA, tmC, a, x, K);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <int LAYOUT, bool VEC>
+cudaError_t launch_fused_sel(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& a, const float* x,
+                             int K, int num_sms, cudaStream_t s) {
+  // weight multicast across CTA pairs needs pairs of units of one batch entry (tiles_n even)
+  const char* env = getenv("TCBF_F16_MC");
+  const bool mc = a.tiles_n % 2 == 0 && a.B * a.tiles_n >= 2 && !(env && atoi(env) == 0);
+  return mc ? launch_fused<LAYOUT, VEC, true>(tmA, tmC, a, x, K, num_sms, s)
+            : launch_fused<LAYOUT, VEC, false>(tmA, tmC, a, x, K, num_sms, s);
 }
 
 }  // namespace
@@ -356,9 +422,9 @@ cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC
                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream) {
   const bool vec = layout == 0 && (args.N % 8 == 0) && (reinterpret_cast<uintptr_t>(x_src) % 16 == 0);
   if (layout == 0)
-    return vec ? launch_fused<0, true>(tmA, tmC, args, x_src, K, num_sms, stream)
-               : launch_fused<0, false>(tmA, tmC, args, x_src, K, num_sms, stream);
-  return launch_fused<1, false>(tmA, tmC, args, x_src, K, num_sms, stream);
+    return vec ? launch_fused_sel<0, true>(tmA, tmC, args, x_src, K, num_sms, stream)
+               : launch_fused_sel<0, false>(tmA, tmC, args, x_src, K, num_sms, stream);
+  return launch_fused_sel<1, false>(tmA, tmC, args, x_src, K, num_sms, stream);
 }
 
 }  // namespace tcbf
