@@ -588,15 +588,21 @@ def test_b1_large_k_exact(tcbf, b1_kernel):
 
 
 # ------------------------------------------------------------------ full-size sampled parity
-def _full_size(tcbf, prec, M, N, K, B, wdist, xdist, seed, batches, rows):
+def _full_size(tcbf, prec, M, N, K, B, wdist, xdist, seed, batches, rows, path="packed"):
+    """path: 'packed' (tcbf_pack + tcbf_beamform), 'raw' (tcbf_beamform_raw) or 'f16i'
+    (tcbf_beamform_f16i on the fp16-rounded interleaved data) -- whichever bench.py times."""
     plan = tcbf.Plan(M, N, K, B, prec)
     wsrc = synth.generate_device(wdist, seed, 0, B, M, K)
     wp = plan.pack(tcbf.WEIGHTS, wsrc)
     del wsrc
     xsrc = synth.generate_device(xdist, seed, 1, B, K, N)
-    xp = plan.pack(tcbf.DATA, xsrc)
+    if path == "raw":
+        y = plan.beamform_raw(wp, xsrc)
+    elif path == "f16i":
+        y = plan.beamform_f16i(wp, xsrc.half())
+    else:
+        y = plan.beamform(wp, plan.pack(tcbf.DATA, xsrc))
     del xsrc
-    y = plan.beamform(wp, xp)
     torch.cuda.synchronize()
     nr = len(rows)
     for b in batches:
@@ -622,6 +628,29 @@ def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
     """BASELINE configs[2]: M=1024, K=512, N=4096, batch=256."""
     _full_size(tcbf, "b1", 1024, 4096, 512, 256, "phase", "adc", synth.SEED_BASE + 2,
                batches=[0, 200, 255], rows=[0, 63, 64, 777, 1023])
+
+
+def test_full_size_square_16384_sampled(tcbf):
+    """BASELINE configs[4] largest square points, fp16 and 1-bit, M=N=K=16384."""
+    for prec in ("f16", "b1"):
+        _full_size(tcbf, prec, 16384, 16384, 16384, 1, "uniform", "uniform", synth.SEED_BASE + 4,
+                   batches=[0], rows=[0, 8191, 16383])
+        torch.cuda.empty_cache()
+
+
+def test_full_size_m32_f16_16384_raw_sampled(tcbf):
+    """BASELINE configs[4] small-beam fp16 point through the streaming-conversion kernel, as
+    bench.py times it (M=32, N=K=16384)."""
+    plan = tcbf.Plan(32, 16384, 16384, 1, "f16")
+    assert plan.raw_variant == "f16_tcgen05_stream_conv_128x128"
+    _full_size(tcbf, "f16", 32, 16384, 16384, 1, "uniform", "uniform", synth.SEED_BASE + 4,
+               batches=[0], rows=[0, 17, 31], path="raw")
+
+
+def test_full_size_radio_f16i_sampled(tcbf):
+    """The radio shape with fp16 interleaved data (bench config radio_f16i, no pack)."""
+    _full_size(tcbf, "f16", 1024, 1024, 256, 256, "phase", "adc", synth.SEED_BASE + 1,
+               batches=[0, 255], rows=[0, 127, 1023], path="f16i")
 
 
 def test_sliced_weight_generation_equals_direct(tcbf):
