@@ -159,7 +159,8 @@ tcbf_status tcbf_steering_weights(const tcbf_plan* plan, const double* positions
  * data X (host, pinned recommended) to the device in batch chunks, packs it,
  * beamforms against the already packed device weights and copies the output back
  * to `out_host`, overlapping copies and compute on internal streams.  Blocks until
- * done.  Device scratch is allocated per call (ALLOC on failure). */
+ * done.  Device scratch comes from the device's default stream-ordered pool, whose release
+ * threshold this call raises so the memory stays cached between calls (ALLOC on failure). */
 tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_packed_dev,
                                const float* x_host, tcbf_src_layout layout, void* out_host);
 
