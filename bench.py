@@ -105,6 +105,18 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
     byts = gemm_bytes(c, fused)
     bw = peaks["hbm"]
     t_ms = gemm_ms * 1e-3
+    if c["prec"] == "b1" and "mma_sync" in variant:
+        # legacy b1 mma.sync (emulated on sm_100a): its register-only peak measured by peaks.cu
+        # (profiles/r01/peaks.json); single-AND form = 4 binary MACs per complex MAC, useful = raw
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01", "peaks.json")) as f:
+                bpeak = float(json.load(f)["peaks"]["b1_mma_sync_and_popc"]["tera_ops_per_s"])
+            bsrc = "measured (peaks.cu register-only mma.sync .and.popc, profiles/r01/peaks.json)"
+        except Exception:
+            bpeak, bsrc = 413.0, "fallback (round-1 peaks.cu measurement)"
+        ach = ops / t_ms / 1e12
+        return dict(bound="b1_mma_sync", achieved=round(ach, 1), peak=bpeak, unit="TOP/s",
+                    frac=round(ach / bpeak, 4), peak_src=bsrc)
     if c["prec"] == "b1" and "popc" in variant:
         alu_peak = 16 * 148 * 1.965e9 * 32 * 2 / 1e12
         ach = ops / t_ms / 1e12

@@ -66,6 +66,7 @@ struct GemmB1Args {
   int kb_per_split;
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
+cudaError_t launch_gemm_b1_mma(const GemmB1Args& args, cudaStream_t stream);  // legacy mma.sync b1 AND
 cudaError_t launch_gemm_b1_2cta(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
                                 cudaStream_t stream);
 bool gemm_b1_f8_supported(int64_t Kw);

@@ -187,6 +187,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     else if (strcmp(env, "f8") == 0 && tcbf::gemm_b1_f8_supported(kp)) p->b1_tc = 2;
     else if (strcmp(env, "i8pair") == 0) p->b1_tc = 3;
     else if (strcmp(env, "f4") == 0 && tcbf::gemm_b1_f4_supported(kp)) p->b1_tc = 4;
+    else if (strcmp(env, "bmma") == 0) p->b1_tc = 5;
   }
   *plan = p;
   return TCBF_OK;
@@ -214,6 +215,7 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (!plan) return "none";
   if (plan->prec == TCBF_PREC_B1) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
+    if (plan->b1_tc == 5) return "b1_mma_sync_and_128x64";
     if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
     if (plan->b1_tc == 3) return plan->N % 4 ? "b1_tcgen05_i8_2cta_256x128_stg" : "b1_tcgen05_i8_2cta_256x128_tma";
     if (plan->b1_tc == 4 && tcbf::gemm_b1_f4_swap_beams(plan->M) && !getenv("TCBF_NO_SWAP"))
@@ -359,7 +361,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
       e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
     }
-    if (plan->b1_tc) {
+    if (plan->b1_tc == 5) {
+      e = tcbf::launch_gemm_b1_mma(a, st);
+    } else if (plan->b1_tc) {
       const bool tma_store = (plan->N % 4) == 0;
       CUtensorMap tc;
       memset(&tc, 0, sizeof(tc));

@@ -13,7 +13,8 @@ struct tcbf_plan_s {
   int num_sms;
   int f16_variant;  // tcbf::F16_V_*
   int64_t n_packed;  // F16 data row length Np = round_up(N, 8) (MN-major packed data)
-  int b1_tc;    // 1-bit kernel: 2 = tensor cores kind::f8f6f4 (+-1), 1 = kind::i8 (AND form), 0 = CUDA-core popc
+  int b1_tc;    // 1-bit kernel: 4 = kind::mxf4 (+-1, default), 3 = kind::i8 CTA pair, 2 = kind::f8f6f4 (+-1),
+                // 1 = kind::i8 (AND form), 5 = legacy mma.sync b1 AND, 0 = CUDA-core popc
   size_t w_bytes, x_bytes, out_bytes;
 };
 

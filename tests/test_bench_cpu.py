@@ -79,3 +79,15 @@ def test_roofline_binding_roof_and_kind():
     assert r4["peak"] == 4 * 1600.0 and r8["peak"] == 2 * 1600.0
     rp = bench.roofline_for(sqb, 1.0, peaks, long_step=False, variant="b1_popc_xor_64x64")
     assert rp["bound"] == "alu"
+    rm = bench.roofline_for(sqb, 1.0, peaks, long_step=False, variant="b1_mma_sync_and_128x64")
+    assert rm["bound"] == "b1_mma_sync" and rm["peak"] > 100.0   # measured peaks.cu value
+
+
+def test_peaks_record_committed():
+    """profiles/r01/peaks.json (peaks.cu on the B200) holds every kind tools/peaks.py measures."""
+    import json
+    with open(os.path.join(ROOT, "profiles", "r01", "peaks.json")) as f:
+        d = json.load(f)["peaks"]
+    for k in ("b1_mma_sync_and_popc", "b1_mma_sync_xor_popc", "cuda_core_xor_popc", "tcgen05_f16", "tcgen05_i8",
+              "tcgen05_mxf4"):
+        assert d[k]["tera_ops_per_s"] > 0
