@@ -140,6 +140,17 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
                 frac=round(ach / tpeak, 4), peak_src=src, hbm_frac=round(byts / t_ms / 1e9 / bw, 4))
 
 
+def pack_roofline(c, pack_ms, packed_bytes, peaks):
+    """tcbf_pack(DATA) as the dominant kernel: HBM-bound stream, algorithmic bytes = the fp32
+    complex source read once (8 B per element) + the packed operand written once."""
+    byts = c["B"] * c["K"] * c["N"] * 8 + packed_bytes
+    ach = byts / (pack_ms * 1e-3) / 1e9
+    bw = peaks["hbm"]
+    return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
+                peak_src=peaks["src"], kernel="pack_b1_transpose" if c["prec"] == "b1" else "pack_f16_rows",
+                kernel_ms=round(pack_ms, 4), algorithmic_bytes_per_launch=byts)
+
+
 def traffic_for(c_name, kernel):
     """dram bytes per launch from the committed ncu --set full capture (profiles/traffic.json) of
     the same config and kernel, or None."""
@@ -471,6 +482,14 @@ def run_tcbf(args, c):
     roof["kernel_ms"] = round(gemm_ms_max, 4)
     roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
     roof["useful_ops_per_launch"] = useful_ops(c)
+    pack_ms_max = max_over_ranks(pack_ms, dev) if not (fused or f16i) else 0.0
+    if pack_ms_max > gemm_ms_max:
+        # the data pack dominates the step (few beams: M=32 sweeps): report ITS roofline as the
+        # dominant kernel, the GEMM's beside it
+        pk = pack_roofline(c, pack_ms_max, plan.x_bytes, peaks)
+        pk["gemm"] = roof
+        pk["traffic"] = traffic_for(args.config, pk["kernel"])
+        roof = pk
 
     line = {
         "metric": "beamforming TeraOps/s (fp16 and 1-bit) at 1/2/4/8 B200 vs roofline",

@@ -31,20 +31,25 @@ constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int BK = 64;
 constexpr int KMAX = 256;                 // resident K rows (K16 <= 256)
-constexpr int A_STAGES = 2;
 constexpr int EPI_WARPS = 4;
 constexpr int CONV_WARPS = 8;
 constexpr int NUM_THREADS = (2 + EPI_WARPS + CONV_WARPS) * 32;
 constexpr int A_BYTES = BM * BK * 2;      // one plane of one A stage
 constexpr int A_STAGE_BYTES = 2 * A_BYTES;
 constexpr int B_PLANE_BYTES = 2 * KMAX * 128;  // 2 column blocks x KMAX rows x 128 B
-constexpr int EPI_BYTES = EPI_WARPS * 2 * 4096;
 constexpr int OFF_B = 0;
 constexpr int OFF_A = 2 * B_PLANE_BYTES;
-constexpr int OFF_EPI = OFF_A + A_STAGES * A_STAGE_BYTES;
-constexpr int BAR_OFFSET = OFF_EPI + EPI_BYTES;
-constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
-static_assert(SMEM_BYTES <= 232448, "smem budget");
+// Two epilogues: TMA stores staged through 32 KB of swizzled smem boxes (2 weight stages fit), or
+// DIRECT 256-bit st.global from registers (no staging), whose freed smem holds a third stage.
+template <bool DIRECT>
+struct FCfg {
+  static constexpr int A_STAGES = DIRECT ? 3 : 2;
+  static constexpr int EPI_BYTES = DIRECT ? 0 : EPI_WARPS * 2 * 4096;
+  static constexpr int OFF_EPI = OFF_A + A_STAGES * A_STAGE_BYTES;
+  static constexpr int BAR_OFFSET = OFF_EPI + EPI_BYTES;
+  static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+  static_assert(SMEM_BYTES <= 232448, "smem budget");
+};
 
 __device__ __forceinline__ uint64_t desc_a128(const void* tile, uint32_t k_byte_off) {
   uint32_t addr = smem_u32(tile) + k_byte_off;
@@ -111,16 +116,18 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
 // MC: CTA pairs (clusters of 2) take adjacent units of the same batch entry, so their weight
 // tiles are identical: each CTA TMA-loads one of the two weight planes and multicasts it to both
 // (half the L2 -> SM weight traffic); both MMA issuers release a stage in both CTAs.
-template <int LAYOUT, bool VEC, bool MC>
+template <int LAYOUT, bool VEC, bool MC, bool DIRECT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cgemm_f16_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                            GemmF16Args args, const float* __restrict__ xsrc, int K) {
+  using C = FCfg<DIRECT>;
+  constexpr int A_STAGES = C::A_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem + OFF_B;  // [2 planes][2 column blocks][KMAX rows][128 B]
   uint8_t* sA = smem + OFF_A;
-  uint8_t* epi_base = smem + OFF_EPI;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
+  uint8_t* epi_base = smem + C::OFF_EPI;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + C::BAR_OFFSET);
   uint64_t* aempty = afull + A_STAGES;
   uint64_t* bfull = aempty + A_STAGES;    // [KMAX / BK]
   uint64_t* bempty = bfull + KMAX / BK;   // [KMAX / BK]
@@ -241,6 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     constexpr int CHUNKS = BN / 32;
+    const bool vec8 = (args.N % 8 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 31) == 0);
     int sbuf = 0;
     int it = 0;
     for (int u = u_first; u < num_units; u += u_step) {
@@ -269,13 +277,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           const uint32_t* vv = v[ch & 1];
           if (args.debug & 1) continue;
-          if (args.debug & 16) {  // experiment: direct 256-bit stores from registers (no smem staging)
+          if constexpr (DIRECT) {  // 256-bit stores straight from registers: thread = row, 128 B each
             const int m = m0 + q * 32 + lane;
             const int nb = n0 + c * 32;
-            if (m < args.M && nb + 32 <= args.N) {
+            if (m < args.M) {
               float* row = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
+              if (vec8 && nb + 32 <= args.N) {
 #pragma unroll
-              for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
+                for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (nb + j < args.N) row[j] = __uint_as_float(vv[j]);
+              }
             }
             continue;
           }
@@ -302,7 +316,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (threadIdx.x == 64) stamp(args.trace, 4 * it + 3);
       }
     }
-    if (threadIdx.x == 64) bulk_wait_group<0>();
+    if (!DIRECT && threadIdx.x == 64) bulk_wait_group<0>();
   } else {
     // ------------------------------------------------------------ converters: fp32 data -> resident B
     const int ct = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..255
@@ -374,10 +388,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int LAYOUT, bool VEC, bool MC>
+template <int LAYOUT, bool VEC, bool MC, bool DIRECT>
 cudaError_t launch_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& a, const float* x,
                          int K, int num_sms, cudaStream_t s) {
-  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC, MC>;
+  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC, MC, DIRECT>;
+  constexpr int SMEM_BYTES = FCfg<DIRECT>::SMEM_BYTES;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = a.B * a.tiles_n;
@@ -410,8 +425,13 @@ cudaError_t launch_fused_sel(const CUtensorMap& tmA, const CUtensorMap& tmC, con
   // weight multicast across CTA pairs needs pairs of units of one batch entry (tiles_n even)
   const char* env = getenv("TCBF_F16_MC");
   const bool mc = a.tiles_n % 2 == 0 && a.B * a.tiles_n >= 2 && !(env && atoi(env) == 0);
-  return mc ? launch_fused<LAYOUT, VEC, true>(tmA, tmC, a, x, K, num_sms, s)
-            : launch_fused<LAYOUT, VEC, false>(tmA, tmC, a, x, K, num_sms, s);
+  const char* denv = getenv("TCBF_F16_DIRECT");
+  const bool direct = denv && atoi(denv) != 0;
+  if (direct)
+    return mc ? launch_fused<LAYOUT, VEC, true, true>(tmA, tmC, a, x, K, num_sms, s)
+              : launch_fused<LAYOUT, VEC, false, true>(tmA, tmC, a, x, K, num_sms, s);
+  return mc ? launch_fused<LAYOUT, VEC, true, false>(tmA, tmC, a, x, K, num_sms, s)
+            : launch_fused<LAYOUT, VEC, false, false>(tmA, tmC, a, x, K, num_sms, s);
 }
 
 }  // namespace

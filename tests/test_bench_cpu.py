@@ -91,3 +91,14 @@ def test_peaks_record_committed():
     for k in ("b1_mma_sync_and_popc", "b1_mma_sync_xor_popc", "cuda_core_xor_popc", "tcgen05_f16", "tcgen05_i8",
               "tcgen05_mxf4"):
         assert d[k]["tera_ops_per_s"] > 0
+
+
+def test_pack_roofline_when_pack_dominates():
+    """M=32 1-bit: the fp32 data pack is the step's dominant kernel; its roofline counts the fp32
+    read plus the packed write."""
+    c = bench.CONFIGS["m32_b1_16384"]
+    peaks = dict(hbm=6000.0, bf16=1600.0, bf16_sus=1300.0, src="test")
+    packed = 2 * c["N"] * (c["K"] // 32) * 4
+    byts = c["K"] * c["N"] * 8 + packed
+    r = bench.pack_roofline(c, byts / 6000e9 * 1e3 / 0.5, packed, peaks)
+    assert r["bound"] == "hbm" and abs(r["frac"] - 0.5) < 1e-3 and r["kernel"] == "pack_b1_transpose"
