@@ -1,5 +1,7 @@
 """Summarise ncu outputs into profiles/<tag>/ (tracked):
-  - launch list CSV (gpu__time_duration per launch) -> per-kernel counts, mean time, share of step
+  - launch list CSV (gpu__time_duration per launch) -> per-kernel counts, mean/median/min/max time,
+    share of the listed time (the list covers the whole bench command: generator, weight pack,
+    warm-up, timed steps and the e2e calls, which run the same kernel on host-pipelined chunks)
   - one --set full capture -> key raw metrics + top stall sites
 Usage: python tools/ncu_summary.py <tag> <config> [gpurun_out prefix]
 """
@@ -39,7 +41,12 @@ def launches(path):
             v *= 1e6
         name = r[ki].split("(")[0].replace("void ", "").replace("tcbf::<unnamed>::", "")
         d[name].append(v)
-    return {k: {"launches": len(v), "mean_us": round(sum(v) / len(v) / 1e3, 3)} for k, v in d.items()}
+    def stats(v):
+        v = sorted(v)
+        return {"launches": len(v), "mean_us": round(sum(v) / len(v) / 1e3, 3),
+                "median_us": round(v[len(v) // 2] / 1e3, 3), "min_us": round(v[0] / 1e3, 3),
+                "max_us": round(v[-1] / 1e3, 3)}
+    return {k: stats(v) for k, v in d.items()}
 
 
 def full(path):
