@@ -12,6 +12,7 @@
 // so both GEMM operands are K-major (what the tcgen05 smem descriptors and TMA want).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -104,21 +105,22 @@ __global__ void pack_b1_rows(const float* __restrict__ src, int64_t B, int64_t M
   }
 }
 
-// data: [B][K][N] -> [B][2][N][Kw]; one thread per (column n, chunk of 32 words = 1024 k):
+// data: [B][K][N] -> [B][2][N][Kw]; one thread per (column n, chunk of `wpt` words = 32 wpt k):
 // the 32 k-rows of a word are read with warp-coalesced 256-byte row segments (consecutive n),
 // all 32 loads of a word in flight; the thread's consecutive words of a row merge in L2
-// (the packed output is 1/64 of the bytes read).
-template <int LAYOUT>
+// (the packed output is 1/64 of the bytes read).  wpt = 32 on large operands; small ones use
+// shorter chunks so that the grid still fills every SM (square 1024^2: 8 CTAs -> 256).
+template <int LAYOUT, int wpt>  // compile-time chunk: a runtime trip count measured 1.3-3.5x slower
 __global__ void __launch_bounds__(128) pack_b1_transpose(const float* __restrict__ src, int64_t B, int64_t K,
                                                          int64_t N, int64_t Kw, uint32_t* __restrict__ dst) {
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   for (int64_t b = blockIdx.z; b < B; b += gridDim.z)
-    for (int64_t w0 = (int64_t)blockIdx.y * 32; w0 < Kw; w0 += (int64_t)gridDim.y * 32) {
+    for (int64_t w0 = (int64_t)blockIdx.y * wpt; w0 < Kw; w0 += (int64_t)gridDim.y * wpt) {
       uint32_t* dr = dst + ((b * 2 + 0) * N + n) * Kw + w0;
       uint32_t* di = dst + ((b * 2 + 1) * N + n) * Kw + w0;
 #pragma unroll 1
-      for (int w = 0; w < 32 && w0 + w < Kw; ++w) {
+      for (int w = 0; w < wpt && w0 + w < Kw; ++w) {
         uint32_t br = 0, bi = 0;
         const int64_t kbase = (w0 + w) * 32;
         if (kbase < K) {
@@ -174,9 +176,23 @@ cudaError_t launch_pack_b1(const float* src, int layout, int operand, int64_t B,
     if (layout == 0) pack_b1_rows<0><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, Kw, dst);
     else pack_b1_rows<1><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, Kw, dst);
   } else {
-    dim3 grid((unsigned)((C + 127) / 128), (unsigned)cap_dim((Kw + 31) / 32), (unsigned)cap_dim(B));
-    if (layout == 0) pack_b1_transpose<0><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst);
-    else pack_b1_transpose<1><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst);
+    // words per thread: 32, cut to 8, 2, 1 while fewer (column, chunk) items than four
+    // full-occupancy waves (148 SMs x 2048 threads) would be launched.  Measured (us): square 1024^2
+    // 41.7 -> 10.6, M=32 N=K=4096 52.6 -> 41, N=K=16384 385 -> 345, radio 1-bit unchanged (644)
+    int wpt = 32;
+    while (wpt > 1 && B * C * ((Kw + wpt - 1) / wpt) < 4LL * 148 * 2048) wpt = wpt == 32 ? 8 : wpt == 8 ? 2 : 1;
+    if (const char* env = getenv("TCBF_PACK_WPT")) wpt = atoi(env);  // experiments: 32, 8, 2 or 1
+    wpt = wpt >= 32 ? 32 : wpt >= 8 ? 8 : wpt >= 2 ? 2 : 1;
+    dim3 grid((unsigned)((C + 127) / 128), (unsigned)cap_dim((Kw + wpt - 1) / wpt), (unsigned)cap_dim(B));
+#define TCBF_PACK_B1_T(L, W) pack_b1_transpose<L, W><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst)
+    if (layout == 0) {
+      if (wpt == 32) TCBF_PACK_B1_T(0, 32); else if (wpt == 8) TCBF_PACK_B1_T(0, 8);
+      else if (wpt == 2) TCBF_PACK_B1_T(0, 2); else TCBF_PACK_B1_T(0, 1);
+    } else {
+      if (wpt == 32) TCBF_PACK_B1_T(1, 32); else if (wpt == 8) TCBF_PACK_B1_T(1, 8);
+      else if (wpt == 2) TCBF_PACK_B1_T(1, 2); else TCBF_PACK_B1_T(1, 1);
+    }
+#undef TCBF_PACK_B1_T
   }
   return cudaGetLastError();
 }

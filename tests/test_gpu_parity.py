@@ -105,6 +105,19 @@ def test_pack_b1_bit_exact(tcbf, layout, shape):
     assert np.array_equal(xp, oracle.pack_b1(conv(x), lay, oracle.DATA, B, K, N, plan.k_packed))
 
 
+@pytest.mark.parametrize("wpt", ["32", "8", "2", "1"])
+@pytest.mark.parametrize("shape", [(1, 3000, 130, 2), (1, 9000, 257, 1)])
+def test_pack_b1_data_chunking_bit_exact(tcbf, shape, wpt, monkeypatch):
+    """Every words-per-thread chunking of the 1-bit data pack (chosen by operand size) gives the
+    oracle's packing: ragged K (partial words, partial chunks), ragged N, batch > 1."""
+    monkeypatch.setenv("TCBF_PACK_WPT", wpt)
+    M, K, N, B = shape
+    x = synth.generate("uniform", 9, 1, B, K, N)
+    plan = tcbf.Plan(M, N, K, B, "b1")
+    xp = plan.pack(tcbf.DATA, _dev(synth.to_interleaved(x))).cpu().numpy().view(np.uint32)
+    assert np.array_equal(xp, oracle.pack_b1(synth.to_interleaved(x), 0, oracle.DATA, B, K, N, plan.k_packed))
+
+
 def test_pack_b1_nan_and_signed_zero(tcbf):
     vals = np.array([np.nan, -0.0, 0.0, -1e-45, 1e-45, -np.inf, np.inf], np.float32)
     K = vals.size
