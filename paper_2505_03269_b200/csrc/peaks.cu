@@ -10,6 +10,8 @@
 //   3  tcgen05.mma kind::f16   M=128 N=256 K=16, fp32 accumulate (smem operands, TMEM D)
 //   4  tcgen05.mma kind::i8    M=128 N=256 K=32, int32 accumulate
 //   5  tcgen05.mma kind::mxf4  M=128 N=256 K=64, block32 unit scales, fp32 accumulate
+//   6  tcgen05.mma kind::f16   M=128 N=64  K=16, A from TMEM (the data-in-TMEM fused variant)
+//   7  tcgen05.mma kind::f16   M=128 N=128 K=16, both operands from smem (the fused kernel's MMA)
 // Ops are counted as 2 per multiply-accumulate (binary MACs for kinds 0-2).  Host entry point:
 // tcbf_peak_run (extern "C"), timed with CUDA events around one launch after a warm-up launch.
 // This library is a measurement tool: it is not on the beamforming path.
@@ -103,7 +105,13 @@ __device__ __forceinline__ void tmem_st_same(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-template <int KIND>  // 3 f16, 4 i8, 5 mxf4
+__device__ __forceinline__ void mma_f16_ts_peak(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 1;" ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc),
+               "r"(idesc)
+               : "memory");
+}
+
+template <int KIND>  // 3 f16, 4 i8, 5 mxf4, 6 f16 A-in-TMEM N=64, 7 f16 N=128
 __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -120,7 +128,7 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
     h ^= h >> 15;
     h *= 0x2C1B3C6Du;
     h ^= h >> 13;
-    if (KIND == 3) h &= 0xBBFFBBFFu;  // clear exponent MSB -> |x| < 2 in both halves
+    if (KIND == 3 || KIND >= 6) h &= 0xBBFFBBFFu;  // clear exponent MSB -> |x| < 2 in both halves
     reinterpret_cast<uint32_t*>(smem)[i] = h;
   }
   if (threadIdx.x == 0) {
@@ -147,13 +155,16 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
   if (threadIdx.x == 0) {
     uint32_t idesc;
     if (KIND == 3) idesc = idesc_f16(128, 256, false);
+    else if (KIND == 6) idesc = idesc_f16(128, 64, false);
+    else if (KIND == 7) idesc = idesc_f16(128, 128, false);
     else if (KIND == 4) idesc = idesc_s8(128, 256);
     else idesc = (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte row
         const uint64_t ad = smem_desc_k128(sA, kk * 32), bd = smem_desc_k128(sB, kk * 32);
-        if (KIND == 3) mma_f16_ss(tmem, ad, bd, idesc, 1u);
+        if (KIND == 3 || KIND == 7) mma_f16_ss(tmem, ad, bd, idesc, 1u);
+        else if (KIND == 6) mma_f16_ts_peak(tmem + 256, tmem + kk * 8, bd, idesc);  // A: columns 0..31
         else if (KIND == 4) mma_i8_ss(tmem, ad, bd, idesc, 1u);
         else mma_mxf4_peak(tmem, ad, bd, idesc, tmem + 256, tmem + 256 + 128);
       }
@@ -188,7 +199,7 @@ extern "C" {
 // -1 for an unknown kind or iters <= 0, else the cudaError_t value.
 __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, double* seconds, double* ops) {
   using namespace tcbf;
-  if (kind < 0 || kind > 5 || iters <= 0 || !seconds || !ops) return -1;
+  if (kind < 0 || kind > 7 || iters <= 0 || !seconds || !ops) return -1;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -214,12 +225,14 @@ __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, do
       peak_popc_kernel<<<blocks, threads>>>(seed, iters, sink);
       work = 2.0 * 32 * 4 * POPC_CHAINS * (double)iters * blocks * threads;
     } else {
-      auto k = kind == 3 ? peak_tc_kernel<3> : kind == 4 ? peak_tc_kernel<4> : peak_tc_kernel<5>;
+      auto k = kind == 3 ? peak_tc_kernel<3> : kind == 4 ? peak_tc_kernel<4> : kind == 5 ? peak_tc_kernel<5>
+             : kind == 6 ? peak_tc_kernel<6> : peak_tc_kernel<7>;
       cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
       if (a != cudaSuccess) return a;
       k<<<sms, 128, TC_SMEM>>>(iters, sink);
-      const double kdim = kind == 3 ? 16 : kind == 4 ? 32 : 64;
-      work = 2.0 * 128 * 256 * kdim * 4 * (double)iters * sms;
+      const double kdim = (kind == 3 || kind >= 6) ? 16 : kind == 4 ? 32 : 64;
+      const double ndim = kind == 6 ? 64 : kind == 7 ? 128 : 256;
+      work = 2.0 * 128 * ndim * kdim * 4 * (double)iters * sms;
     }
     return cudaGetLastError();
   };

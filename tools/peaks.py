@@ -28,9 +28,11 @@ KINDS = {
     3: ("tcgen05_f16", "tcgen05.mma kind::f16 128x256x16, fp32 acc", 1.0),
     4: ("tcgen05_i8", "tcgen05.mma kind::i8 128x256x32, int32 acc", 1.0),
     5: ("tcgen05_mxf4", "tcgen05.mma kind::mxf4 block32 128x256x64, fp32 acc", 1.0),
+    6: ("tcgen05_f16_ts_n64", "tcgen05.mma kind::f16 128x64x16, A from TMEM", 1.0),
+    7: ("tcgen05_f16_ss_n128", "tcgen05.mma kind::f16 128x128x16, A and B from smem", 1.0),
 }
 # iterations per warp / issuing thread: each launch runs ~5-50 ms
-ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000}
+ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000, 6: 80000, 7: 80000}
 
 
 def clocks():
