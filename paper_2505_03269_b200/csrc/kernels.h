@@ -77,6 +77,8 @@ int gemm_b1_f4_store_box_cols(int64_t Kw);
 int gemm_b1_f4_swap_beams(int64_t M);  // beams per tile of the swapped small-M kernel (0: not used)
 cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                    const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
+cudaError_t launch_gemm_b1_f4_2cta(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
+                                   cudaStream_t stream);
 cudaError_t launch_gemm_b1_f4(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                               const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
 bool gemm_b1_fused_supported(int64_t Kw, int64_t N);

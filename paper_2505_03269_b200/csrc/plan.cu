@@ -188,6 +188,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
     else if (strcmp(env, "i8pair") == 0) p->b1_tc = 3;
     else if (strcmp(env, "f4") == 0 && tcbf::gemm_b1_f4_supported(kp)) p->b1_tc = 4;
     else if (strcmp(env, "bmma") == 0) p->b1_tc = 5;
+    else if (strcmp(env, "f4pair") == 0 && tcbf::gemm_b1_f4_supported(kp)) p->b1_tc = 6;
   }
   *plan = p;
   return TCBF_OK;
@@ -216,6 +217,8 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (plan->prec == TCBF_PREC_B1) {
     if (!plan->b1_tc) return "b1_popc_xor_64x64";
     if (plan->b1_tc == 5) return "b1_mma_sync_and_128x64";
+    if (plan->b1_tc == 6)
+      return plan->N % 4 ? "b1_tcgen05_mxf4pm1_2cta_256x128_stg" : "b1_tcgen05_mxf4pm1_2cta_256x128_tma";
     if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
     if (plan->b1_tc == 3) return plan->N % 4 ? "b1_tcgen05_i8_2cta_256x128_stg" : "b1_tcgen05_i8_2cta_256x128_tma";
     if (plan->b1_tc == 4 && tcbf::gemm_b1_f4_swap_beams(plan->M) && !getenv("TCBF_NO_SWAP"))
@@ -372,13 +375,15 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (s != TCBF_OK) return s;
       }
-      if (plan->b1_tc == 3) {  // CTA pair: 256-row pair tiles
+      if (plan->b1_tc == 3 || plan->b1_tc == 6) {  // CTA pair: 256-row pair tiles
         const int64_t bpr = 256 * plan->kp * 8;
         a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bpr, (plan->M + 255) / 256));
       }
       const int swap_tm = plan->b1_tc == 4 && getenv("TCBF_NO_SWAP") == nullptr
                               ? tcbf::gemm_b1_f4_swap_beams(plan->M) : 0;
-      if (swap_tm) {  // few beams: samples on the 128-row MMA dimension, beams on N
+      if (plan->b1_tc == 6) {
+        e = tcbf::launch_gemm_b1_f4_2cta(tc, a, tma_store, plan->num_sms, st);
+      } else if (swap_tm) {  // few beams: samples on the 128-row MMA dimension, beams on N
         CUtensorMap tw, tx;
         const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
         s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw,

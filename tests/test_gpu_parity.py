@@ -492,7 +492,7 @@ def test_abi_errors_on_device(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
-@pytest.fixture(params=["f4", "f8", "i8", "i8pair", "popc", "bmma"])
+@pytest.fixture(params=["f4", "f4pair", "f8", "i8", "i8pair", "popc", "bmma"])
 def b1_kernel(request, monkeypatch):
     """All 1-bit kernels: tcgen05 kind::mxf4 (default) and kind::f8f6f4 on +-1, tcgen05 kind::i8
     AND form (1-CTA and CTA pair), the CUDA-core XOR/popc kernel and the legacy b1 mma.sync
@@ -511,8 +511,8 @@ def test_b1_beamform_bit_exact(tcbf, shape, b1_kernel):
     w = synth.generate("adc", 31, 0, B, M, K)
     x = synth.generate("adc", 31, 1, B, K, N)
     plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
-    assert {"f4": "mxf4", "f8": "f8pm1", "i8pair": "2cta", "popc": "popc", "bmma": "mma_sync"}.get(
-        b1_kernel, "i8") in plan.variant
+    assert {"f4": "mxf4", "f4pair": "mxf4pm1_2cta", "f8": "f8pm1", "i8pair": "2cta", "popc": "popc",
+            "bmma": "mma_sync"}.get(b1_kernel, "i8") in plan.variant
     ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
     assert np.array_equal(y, ref)
     refp = oracle.cgemm_b1_packed(wp.cpu().numpy().view(np.uint32), xp.cpu().numpy().view(np.uint32),
