@@ -23,7 +23,8 @@
 // so it is opt-in (TCBF_B1_KERNEL=f4pair): with MMAs and expansion both skipped (TCBF_DEBUG=6) the
 // pair's skeleton -- register look-ahead word loads plus the per-K-block cluster barrier round trip
 // -- already takes 1.05 ms against 0.44 ms for the 1-CTA kernel's TMA-fed skeleton; a third stage
-// made it slower (1.60 ms).  Bit-exact (tests/test_gpu_parity.py, b1_kernel = f4pair).
+// made it slower (1.60 ms); without word loads (TCBF_DEBUG bit 3) the full pipeline still takes 0.92 ms.
+// Bit-exact (tests/test_gpu_parity.py, b1_kernel = f4pair).
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint4* li = nullptr;
     if (lt < num_tiles) row_ptrs(lt, lr, li);
     auto load_next = [&](uint4 (&d)[4]) {
-      const bool ok = lr != nullptr;
+      const bool ok = lr != nullptr && !(p.debug & 8);  // ablation bit 3: no word loads
       d[0] = ok ? __ldg(lr + 2 * lkb) : zero;
       d[1] = ok ? __ldg(lr + 2 * lkb + 1) : zero;
       d[2] = ok ? __ldg(li + 2 * lkb) : zero;
