@@ -225,7 +225,12 @@ const char* tcbf_plan_variant(const tcbf_plan* plan) {
       return tcbf::gemm_b1_f4_swap_beams(plan->M) == 32
                  ? (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x32_stg" : "b1_tcgen05_mxf4pm1_swap_128x32_tma")
                  : (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x64_stg" : "b1_tcgen05_mxf4pm1_swap_128x64_tma");
-    if (plan->b1_tc == 4) return plan->N % 4 ? "b1_tcgen05_mxf4pm1_128x128_stg" : "b1_tcgen05_mxf4pm1_128x128_tma";
+    if (plan->b1_tc == 4) {
+      const char* at = getenv("TCBF_B1_ATMEM");
+      if (at && atoi(at) == 0)
+        return plan->N % 4 ? "b1_tcgen05_mxf4pm1_128x128_stg" : "b1_tcgen05_mxf4pm1_128x128_tma";
+      return plan->N % 4 ? "b1_tcgen05_mxf4pm1_atmem_128x128_stg" : "b1_tcgen05_mxf4pm1_atmem_128x128_tma";
+    }
     return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
   }
   static const char* names[tcbf::F16_V_COUNT] = {
