@@ -23,7 +23,13 @@ SHAPES = [  # name, prec, M, N, K, B, wdist, xdist
     ("square_b1_8192", "b1", 8192, 8192, 8192, 1, "uniform", "uniform"),
 ]
 F16_VARIANTS = {"1cta_k64s3": "1", "1cta_coop": "11", "1cta_k32s4e8": "0", "2cta_256x128": "7", "2cta_256x256": "8"}
-B1_VARIANTS = ["f4", "i8", "f8", "i8pair"]
+# 1-bit: fp4 with weights in TMEM (default), fp4 all-smem, fp4 CTA pair, int8, fp8, int8 pair,
+# legacy b1 mma.sync, CUDA-core popc
+B1_VARIANTS = {"f4": {"TCBF_B1_KERNEL": "f4"}, "f4_smem": {"TCBF_B1_KERNEL": "f4", "TCBF_B1_ATMEM": "0"},
+               "f4pair": {"TCBF_B1_KERNEL": "f4pair"}, "i8": {"TCBF_B1_KERNEL": "i8"},
+               "f8": {"TCBF_B1_KERNEL": "f8"}, "i8pair": {"TCBF_B1_KERNEL": "i8pair"},
+               "bmma": {"TCBF_B1_KERNEL": "bmma"}, "popc": {"TCBF_B1_KERNEL": "popc"}}
+ENV_KEYS = ("TCBF_F16_VARIANT", "TCBF_B1_KERNEL", "TCBF_B1_ATMEM")
 
 
 def energy_mj():
@@ -74,11 +80,11 @@ def main():
                 variants.append(("fused_raw (pack+gemm)", {}, "raw"))
             variants.append(("pack+gemm default", {}, "two"))
         else:
-            for v in B1_VARIANTS:
-                variants.append((v, {"TCBF_B1_KERNEL": v}, "gemm"))
+            for v, env in B1_VARIANTS.items():
+                variants.append((v, env, "gemm"))
         ref = None
         for vname, env, mode in variants:
-            for k in ("TCBF_F16_VARIANT", "TCBF_B1_KERNEL"):
+            for k in ENV_KEYS:
                 os.environ.pop(k, None)
             os.environ.update(env)
             plan = tcbf.Plan(M, N, K, B, prec)
@@ -100,7 +106,7 @@ def main():
                    "watts": round(j / (ms * 1e-3), 0) if j else None, "bit_identical_to_first": same}
             rows.append(row)
             print(json.dumps(row), flush=True)
-        for k in ("TCBF_F16_VARIANT", "TCBF_B1_KERNEL"):
+        for k in ENV_KEYS:
             os.environ.pop(k, None)
         del wp, x, xp, out
         torch.cuda.empty_cache()
