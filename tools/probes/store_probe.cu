@@ -38,6 +38,34 @@ __global__ void __launch_bounds__(128, 1) tma_store_kernel(const __grid_constant
   }
 }
 
+// per-warp issue (as the 1-bit / fp16 epilogues): each of W warps stores 32-row x 32-column boxes of
+// its own 32-row quarter, with up to INFL boxes in flight per warp
+template <int W, int INFL>
+__global__ void __launch_bounds__(W * 32, 1) tma_store_warps_kernel(const __grid_constant__ CUtensorMap tmC, int B,
+                                                                   int M, int N) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = M / 128, tiles_n = N / 128;
+  const int num_tiles = B * tiles_m * tiles_n;
+  uint8_t* bufs = smem + warp * INFL * 4096;
+  int buf = 0;
+  if (lane == 0) {
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int b = t / (tiles_m * tiles_n), r = t % (tiles_m * tiles_n);
+      const int mt = r % tiles_m, nt = r / tiles_m;
+      // this warp's share of the tile's 2 planes x 4 row quarters x 4 column chunks of 32
+      for (int i = warp; i < 32; i += W) {
+        const int part = i >> 4, q = (i >> 2) & 3, c = i & 3;
+        bulk_wait_group_read<INFL - 1>();
+        tma_store_3d(&tmC, bufs + buf * 4096, nt * 128 + c * 32, mt * 128 + q * 32, 2 * b + part);
+        bulk_commit_group();
+        buf = (buf + 1) % INFL;
+      }
+    }
+    bulk_wait_group<0>();
+  }
+}
 __global__ void vec_store_kernel(float4* out, size_t n4) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -102,6 +130,21 @@ int main() {
     auto k = tma_store_kernel<32, 32>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 4096 + 1024);
     run("TMA box 32c x 32r swz128", [&] { k<<<sms, 128, 4 * 4096 + 1024>>>(m, B, M, N, 0); });
+  }
+  {
+    CUtensorMap m = make_map(32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+    auto k1 = tma_store_warps_kernel<8, 2>;
+    auto k2 = tma_store_warps_kernel<8, 4>;
+    auto k3 = tma_store_warps_kernel<8, 6>;
+    auto k4 = tma_store_warps_kernel<16, 4>;
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 2 * 4096 + 1024);
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4 * 4096 + 1024);
+    cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 6 * 4096 + 1024);
+    cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * 4 * 4096 + 1024);
+    run("TMA 32x32 boxes, 8 warps x 2 in flight", [&] { k1<<<sms, 256, 8 * 2 * 4096 + 1024>>>(m, B, M, N); });
+    run("TMA 32x32 boxes, 8 warps x 4 in flight", [&] { k2<<<sms, 256, 8 * 4 * 4096 + 1024>>>(m, B, M, N); });
+    run("TMA 32x32 boxes, 8 warps x 6 in flight", [&] { k3<<<sms, 256, 8 * 6 * 4096 + 1024>>>(m, B, M, N); });
+    run("TMA 32x32 boxes, 16 warps x 4 in flight", [&] { k4<<<sms, 512, 16 * 4 * 4096 + 1024>>>(m, B, M, N); });
   }
   return 0;
 }
