@@ -105,8 +105,9 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
  * w_packed / x_packed: buffers written by tcbf_pack (16-byte aligned);
  * out: tcbf_output_bytes() bytes, 16-byte aligned, must not overlap the inputs.
  * F16: fp32 result of fp16 inputs with fp32 accumulation (tcgen05 tensor cores).
- * B1:  exact int32 result (the packed bits are expanded to +-1 in shared memory and multiplied
- *      on the fp4 tensor cores, exact for K <= 2^23, int8 tensor cores beyond).
+ * B1:  exact int32 result (the packed bits are expanded to +-1 -- weights into tensor memory,
+ *      data into shared memory -- and multiplied on the fp4 tensor cores, exact for K <= 2^23,
+ *      int8 tensor cores beyond).
  * One launch, or two (memset + kernel) when a split-K variant is forced.  One call may be in
  * flight per (plan, out) pair; the plan itself is stateless and may be used from several streams. */
 tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed,
