@@ -77,7 +77,13 @@ tcbf_status tcbf_layout_sizes(int64_t M, int64_t N, int64_t K, int64_t batch,
 /* Create an immutable plan for batch x (M beams, N samples, K receivers).
  * Host-only validation as tcbf_layout_sizes, then binds the current device,
  * which must be compute capability 10.0 (else UNSUPPORTED_DEVICE).  *plan is
- * set to NULL on failure.  The plan owns only host metadata. */
+ * set to NULL on failure.  The plan owns only host metadata.
+ * The kernel every entry point will run is chosen here, from the shape (DESIGN.md §4 policy).
+ * Experiment overrides are read from the environment HERE ONLY (TCBF_F16_VARIANT,
+ * TCBF_B1_KERNEL=f4|i8|bmma|popc, TCBF_NO_SWAP, TCBF_B1_SPLITS, TCBF_NO_FUSED,
+ * TCBF_FORCE_STREAM_CONV, TCBF_CONV_SPLITS, TCBF_F16_MC, TCBF_PACK_WPT); every variant they
+ * select computes the same result (1-bit: bit-exact; 16-bit: within the fp32 summation-order
+ * tolerance), and a plan never reads the environment again. */
 tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, int64_t batch,
                              tcbf_precision precision);
 
@@ -97,7 +103,11 @@ tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes);
  * B1 DATA is transposed to [B][2][N][Kp] (bits run along K); F16 DATA keeps the
  * [K][N] order (the GEMM reads it MN-major).  src must be 8-byte
  * aligned (interleaved) or 4-byte aligned (planar); dst 16-byte aligned.
- * dst and src must not overlap. */
+ * dst and src must not overlap.
+ * Non-finite inputs are NOT rejected (a deliberate deviation from SPEC.md:50-52, which reports the
+ * first offending index): F16 keeps IEEE semantics (inf/NaN propagate, |x| > 65504 rounds to inf)
+ * and B1 maps NaN to bit 0 (-1) because NaN >= 0 is false (readings R4, R5).  Validate
+ * sources upstream when they may hold non-finite values; the pack stays a single streaming pass. */
 tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src,
                       tcbf_src_layout layout, void* dst, void* stream);
 
@@ -169,8 +179,25 @@ tcbf_status tcbf_beamform_host(const tcbf_plan* plan, const void* w_packed_dev,
  * issued (for launch accounting in benchmarks). */
 int tcbf_last_launch_count(void);
 
-/* Name of the kernel variant the plan dispatches to (static string). */
+/* Name of the kernel tcbf_beamform launches for this plan (static string; "none" for NULL). */
 const char* tcbf_plan_variant(const tcbf_plan* plan);
+
+/* Entry points, for tcbf_plan_kernel. */
+typedef enum {
+  TCBF_ENTRY_BEAMFORM = 0,      /* tcbf_beamform */
+  TCBF_ENTRY_BEAMFORM_RAW = 1,  /* tcbf_beamform_raw (16-byte-aligned source) */
+  TCBF_ENTRY_BEAMFORM_F16I = 2  /* tcbf_beamform_f16i */
+} tcbf_entry;
+
+/* Name of the GEMM kernel `entry` launches for this plan (static string; "none" for a NULL plan
+ * or an entry the plan's precision does not support).  For tcbf_beamform_raw on plans without a
+ * fused kernel this is the GEMM that follows the pack kernel.  The choice is made once, at plan
+ * creation, and never changes: callers (benchmarks) can label measurements with it. */
+const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry);
+
+/* 1 if tcbf_beamform_raw converts the data inside the GEMM for this plan (one kernel, no separate
+ * pack pass; 16-byte-aligned source), 0 if it packs into scratch and then beamforms. */
+int tcbf_plan_raw_fused(const tcbf_plan* plan);
 
 const char* tcbf_status_string(tcbf_status status);
 const char* tcbf_last_error(void);

@@ -73,6 +73,10 @@ def lib():
         L.tcbf_last_launch_count.argtypes = []
         L.tcbf_plan_variant.restype = ctypes.c_char_p
         L.tcbf_plan_variant.argtypes = [vp]
+        L.tcbf_plan_kernel.restype = ctypes.c_char_p
+        L.tcbf_plan_kernel.argtypes = [vp, ctypes.c_int]
+        L.tcbf_plan_raw_fused.restype = ctypes.c_int
+        L.tcbf_plan_raw_fused.argtypes = [vp]
         L.tcbf_status_string.restype = ctypes.c_char_p
         L.tcbf_status_string.argtypes = [ctypes.c_int]
         L.tcbf_last_error.restype = ctypes.c_char_p
@@ -98,17 +102,28 @@ def layout_sizes(M, N, K, batch, precision="f16"):
     return w.value, x.value, o.value, k.value
 
 
-def _conv_splits(tiles, num_kb, num_sms):
-    """K split of the streaming-conversion kernel (mirror of gemm_f16_conv_splits in gemm_f16_conv.cu)."""
-    if tiles <= 0 or num_sms <= 0 or tiles * 5 >= num_sms * 3:
-        return 1
-    s = (num_sms * 85 // 100 + tiles - 1) // tiles
-    return max(1, min(s, 16, num_kb // 16))
-
-
-def _num_sms():
+def _dtype(name):
     import torch
-    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return {"f32": torch.float32, "f16": torch.float16, "i32": torch.int32}[name]
+
+
+def _need(t, what, dtypes, nbytes, device=None):
+    """Argument check before a raw pointer crosses the ABI (the C side cannot see tensor
+    metadata): CUDA tensor, contiguous, one of `dtypes`, at least `nbytes` bytes, on `device`."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{what}: expected a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ValueError(f"{what}: must be a CUDA tensor (got device {t.device})")
+    if device is not None and t.device != device:
+        raise ValueError(f"{what}: on {t.device}, expected {device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what}: must be contiguous")
+    if t.dtype not in tuple(_dtype(d) for d in dtypes):
+        raise TypeError(f"{what}: dtype {t.dtype} not in {dtypes}")
+    have = t.numel() * t.element_size()
+    if have < nbytes:
+        raise ValueError(f"{what}: {have} bytes < the plan's {nbytes}")
 
 
 def _stream_ptr(stream, device):
@@ -161,18 +176,37 @@ class Plan:
         dt = torch.float32 if self.precision == F16 else torch.int32
         return torch.empty((self.batch, 2, self.M, self.N), dtype=dt, device=device)
 
+    # ------------------------------------------------------------ argument checks
+    def _src_bytes(self, operand):
+        rows, cols = (self.M, self.K) if operand == WEIGHTS else (self.K, self.N)
+        return self.batch * rows * cols * 8
+
+    def _packed_bytes(self, operand):
+        return self.w_bytes if operand == WEIGHTS else self.x_bytes
+
+    def _packed_dtypes(self):
+        return ("f16",) if self.precision == F16 else ("i32",)
+
+    def _out_dtype(self):
+        return ("f32",) if self.precision == F16 else ("i32",)
+
     # ------------------------------------------------------------ the path
     def pack(self, operand, src, layout="interleaved", out=None, stream=None):
         lay = _LAYOUT[layout]
+        _need(src, "pack source", ("f32",), self._src_bytes(operand))
         if out is None:
             out = self.alloc_packed(operand, src.device)
+        _need(out, "packed output", self._packed_dtypes(), self._packed_bytes(operand), src.device)
         _check(lib().tcbf_pack(self._h, int(operand), ctypes.c_void_p(src.data_ptr()), lay,
                                ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream, src.device)), "tcbf_pack")
         return out
 
     def beamform(self, w_packed, x_packed, out=None, stream=None):
+        _need(w_packed, "packed weights", self._packed_dtypes(), self.w_bytes)
+        _need(x_packed, "packed data", self._packed_dtypes(), self.x_bytes, w_packed.device)
         if out is None:
             out = self.alloc_output(w_packed.device)
+        _need(out, "output", self._out_dtype(), self.out_bytes, w_packed.device)
         _check(lib().tcbf_beamform(self._h, ctypes.c_void_p(w_packed.data_ptr()),
                                    ctypes.c_void_p(x_packed.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                    _stream_ptr(stream, w_packed.device)), "tcbf_beamform")
@@ -180,8 +214,11 @@ class Plan:
 
     def beamform_raw(self, w_packed, x_src, layout="interleaved", out=None, stream=None):
         """Beamform straight from the fp32 data (pack fused into the GEMM where supported)."""
+        _need(w_packed, "packed weights", self._packed_dtypes(), self.w_bytes)
+        _need(x_src, "data source", ("f32",), self._src_bytes(DATA), w_packed.device)
         if out is None:
             out = self.alloc_output(w_packed.device)
+        _need(out, "output", self._out_dtype(), self.out_bytes, w_packed.device)
         _check(lib().tcbf_beamform_raw(self._h, ctypes.c_void_p(w_packed.data_ptr()),
                                        ctypes.c_void_p(x_src.data_ptr()), _LAYOUT[layout],
                                        ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream, w_packed.device)),
@@ -191,48 +228,43 @@ class Plan:
     def beamform_f16i(self, w_packed, x_f16, out=None, stream=None):
         """16-bit beamform of fp16 interleaved complex data x_f16 [B][K][N][2] (torch.float16, cuda),
         no data pack (NEXT-1)."""
+        _need(w_packed, "packed weights", self._packed_dtypes(), self.w_bytes)
+        _need(x_f16, "fp16 interleaved data", ("f16",), self.batch * self.K * self.N * 4, w_packed.device)
         if out is None:
             out = self.alloc_output(w_packed.device)
+        _need(out, "output", self._out_dtype(), self.out_bytes, w_packed.device)
         _check(lib().tcbf_beamform_f16i(self._h, ctypes.c_void_p(w_packed.data_ptr()),
                                         ctypes.c_void_p(x_f16.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                         _stream_ptr(stream, w_packed.device)), "tcbf_beamform_f16i")
         return out
 
+    def kernel(self, entry="beamform") -> str:
+        """Name of the GEMM kernel an entry point launches for this plan (chosen by the C library
+        at plan creation; entry: 'beamform' | 'raw' | 'f16i')."""
+        e = {"beamform": 0, "raw": 1, "f16i": 2}[entry]
+        return lib().tcbf_plan_kernel(self._h, e).decode()
+
     @property
     def raw_fused(self) -> bool:
-        """True when beamform_raw runs the fused single-kernel path for this plan."""
-        if self.precision == B1:   # fused 1-bit kernel: int8 variant, opt-in (TCBF_B1_FUSED=1, TCBF_B1_KERNEL=i8)
-            return (self.k_packed <= 16 and self.N % 4 == 0 and os.environ.get("TCBF_B1_KERNEL") == "i8"
-                    and "TCBF_B1_FUSED" in os.environ)
-        if self.N % 4:
-            return False
-        if self.k_packed <= 256:
-            return True
-        tiles = (self.N + 127) // 128 * self.batch
-        units = tiles * _conv_splits(tiles, (self.K + 31) // 32, _num_sms())
-        return self.M <= 128 and (units >= _num_sms() // 4 or "TCBF_FORCE_STREAM_CONV" in os.environ)
+        """True when beamform_raw runs one kernel with the data conversion inside (no pack pass)."""
+        return bool(lib().tcbf_plan_raw_fused(self._h))
 
     @property
     def raw_variant(self) -> str:
-        """Kernel that beamform_raw launches for this plan (mirror of the dispatch in plan.cu)."""
-        if not self.raw_fused:
-            return self.variant
-        if self.precision == B1:
-            return "b1_tcgen05_i8_fused_pack_128x128"
-        if self.k_packed <= 256:
-            units = (self.N + 127) // 128 * self.batch
-            if self.M >= 256 and units >= 2 and os.environ.get("TCBF_F16_FUSED") == "2":
-                return "f16_tcgen05_fused_pack_bres_2cta_256x128"
-            return "f16_tcgen05_fused_pack_bres_128x128"
-        return "f16_tcgen05_stream_conv_128x128"
+        return self.kernel("raw")
 
     def steering_weights(self, positions, angles, freqs, c, layout="interleaved", out=None, stream=None):
         """fp32 weight source w[b][m][k] = exp(+2 pi i f_b d_k sin(theta_m) / c).
         positions [K], angles [M], freqs [B]: cuda float64 tensors."""
         import torch
+        for t, what, n in ((positions, "positions", self.K), (angles, "angles", self.M), (freqs, "freqs", self.batch)):
+            if not isinstance(t, torch.Tensor) or t.dtype != torch.float64:
+                raise TypeError(f"{what}: expected a float64 torch.Tensor")
+            _need(t.view(torch.float32), what, ("f32",), 8 * n, positions.device)
         if out is None:
             shape = (self.batch, self.M, self.K, 2) if _LAYOUT[layout] == INTERLEAVED else (self.batch, 2, self.M, self.K)
             out = torch.empty(shape, dtype=torch.float32, device=positions.device)
+        _need(out, "weight source", ("f32",), self._src_bytes(WEIGHTS), positions.device)
         _check(lib().tcbf_steering_weights(self._h, ctypes.c_void_p(positions.data_ptr()),
                                            ctypes.c_void_p(angles.data_ptr()), ctypes.c_void_p(freqs.data_ptr()),
                                            float(c), _LAYOUT[layout], ctypes.c_void_p(out.data_ptr()),
@@ -241,6 +273,14 @@ class Plan:
 
     def beamform_host(self, w_packed_dev, x_host, out_host, layout="interleaved"):
         """End-to-end over host buffers (torch CPU tensors, pinned for overlap)."""
+        import torch
+        _need(w_packed_dev, "packed weights", self._packed_dtypes(), self.w_bytes)
+        for t, what, dts, nb in ((x_host, "host data", (torch.float32,), self._src_bytes(DATA)),
+                                 (out_host, "host output", (_dtype(self._out_dtype()[0]),), self.out_bytes)):
+            if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_contiguous() or t.dtype not in dts:
+                raise ValueError(f"{what}: must be a contiguous CPU tensor of dtype {dts[0]}")
+            if t.numel() * t.element_size() < nb:
+                raise ValueError(f"{what}: {t.numel() * t.element_size()} bytes < the plan's {nb}")
         _check(lib().tcbf_beamform_host(self._h, ctypes.c_void_p(w_packed_dev.data_ptr()),
                                         ctypes.c_void_p(x_host.data_ptr()), _LAYOUT[layout],
                                         ctypes.c_void_p(out_host.data_ptr())), "tcbf_beamform_host")

@@ -45,17 +45,43 @@ def _run(cmd, log):
         raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ... (log {log})")
 
 
-def build_tcbf(force=False):
+def _compile_objects(srcs, objdir, extra, jobs):
+    """nvcc -c every translation unit in parallel (one process per file), return the objects."""
+    import concurrent.futures as cf
+    os.makedirs(objdir, exist_ok=True)
+    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(ROOT, "include", "tcbf.h")]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if _stale(obj, [src] + hdrs):
+            flags = [f for f in NVCC_FLAGS if f != "-shared"]
+            cmd = [_nvcc(), *ARCH, *flags, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+                   "-c", "-o", obj, src]
+            _run(cmd, obj[:-2] + ".log")
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        return list(ex.map(one, srcs))
+
+
+def build_tcbf(force=False, dev=False):
+    """libtcbf.so (product).  dev=True builds libtcbf_dev.so with the TCBF_DEV ablation switches
+    (DESIGN.md §4 studies); the binding never loads it unless a tool points library_path at it."""
     os.makedirs(LIBDIR, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     srcs = [s for s in srcs if not s.endswith("peaks.cu")]
-    deps = srcs + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        [os.path.join(ROOT, "include", "tcbf.h")]
-    out = os.path.join(LIBDIR, "libtcbf.so")
-    if force or _stale(out, deps):
-        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-               "-o", out, *srcs, "-cudart=static"]
-        _run(cmd, os.path.join(LIBDIR, "build_tcbf.log"))
+    name = "libtcbf_dev.so" if dev else "libtcbf.so"
+    out = os.path.join(LIBDIR, name)
+    objdir = os.path.join(LIBDIR, "obj_dev" if dev else "obj")
+    if force:
+        for o in glob.glob(os.path.join(objdir, "*.o")):
+            os.remove(o)
+    objs = _compile_objects(srcs, objdir, ["-DTCBF_DEV"] if dev else [], jobs=max(1, os.cpu_count() or 1))
+    if force or _stale(out, objs):
+        cmd = [_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-o", out, *objs,
+               "-cudart=static"]
+        _run(cmd, os.path.join(LIBDIR, "build_" + name[:-3] + ".log"))
     return out
 
 
@@ -92,5 +118,8 @@ def build_all(force=False):
 
 
 if __name__ == "__main__":
-    for p in build_all(force="--force" in sys.argv):
-        print(p)
+    if "--dev" in sys.argv:
+        print(build_tcbf(force="--force" in sys.argv, dev=True))
+    else:
+        for p in build_all(force="--force" in sys.argv):
+            print(p)

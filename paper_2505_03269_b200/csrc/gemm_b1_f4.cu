@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t b_ri = smem_desc_k128(sBr, off);  // [B_r; B_i]
             const uint64_t b_nr = smem_desc_k128(sBn, off);  // [-B_i; B_r]
             const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (p.debug & 2) continue;
+            if (TCBF_ABLATE(p, 2)) continue;
             if constexpr (ATMEM) {  // K = 64 nibbles = 8 TMEM columns per MMA
               mma_mxf4_ts(d, ta + kk * 8, b_ri, IDESC, sfa, sfb, acc);
               mma_mxf4_ts(d, ta + 32 + kk * 8, b_nr, IDESC, sfa, sfb, 1u);
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_after();
       // ablation (TCBF_DEBUG bit 3; timing only, wrong values): release TMEM before reading it.
       // Measured upper bound of any early-release epilogue: +3-5% (square 8192^3 0.82 -> 0.79 ms)
-      if ((p.debug & 8) && lane == 0) mbar_arrive(tempty_bar);
+      if ((TCBF_ABLATE(p, 8)) && lane == 0) mbar_arrive(tempty_bar);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + part * BN;
       const int corr = part == 0 ? 0 : two_kpad;
       uint32_t vbuf[2][32];
@@ -318,12 +318,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {  // all TMEM reads of this warp done: the next tile's MMAs may start
           tc_fence_before();
           __syncwarp();
-          if (lane == 0 && !(p.debug & 8)) mbar_arrive(tempty_bar);
+          if (lane == 0 && !(TCBF_ABLATE(p, 8))) mbar_arrive(tempty_bar);
         }
         uint32_t* vv = vbuf[c & 1];
 #pragma unroll
         for (int j = 0; j < 32; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
-        if (p.debug & 1) continue;
+        if (TCBF_ABLATE(p, 1)) continue;
         if constexpr (TMA_STORE) {  // 32-row boxes of BOX_COLS columns, double-buffered per warp
 #pragma unroll
           for (int h = 0; h < 32 / BOX_COLS; ++h) {
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     auto expand_block = [&](const uint4& r0, const uint4& r1, const uint4& i0, const uint4& i1) {
       mbar_wait(&empty_bar[stage], phase ^ 1);
       uint8_t* st = smem + stage * C::STAGE;
-      if (!(p.debug & 4)) {
+      if (!(TCBF_ABLATE(p, 4))) {
         if (a_side) {
           if constexpr (ATMEM) {
             tc_fence_after();
@@ -527,21 +527,13 @@ int gemm_b1_f4_store_box_cols(int64_t Kw) { return gemm_b1_f4_tma_words(Kw) ? 16
 
 cudaError_t launch_gemm_b1_f4(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                               const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream) {
-  // weights in TMEM by default (measured: square 8192^3 0.816 -> 0.700 ms, 16384^3 6.34 -> 5.49 ms,
-  // radio 1.600 -> 1.572 ms; all smem-resident with TCBF_B1_ATMEM=0)
-  const char* env = getenv("TCBF_B1_ATMEM");
-  if (!(env && atoi(env) == 0)) {
-    if (gemm_b1_f4_tma_words(args.Kw))
-      return tma_store ? launch_f4<true, true, true>(tmW, tmX, tmC, args, num_sms, stream)
-                       : launch_f4<false, true, true>(tmW, tmX, tmC, args, num_sms, stream);
-    return tma_store ? launch_f4<true, false, true>(tmW, tmX, tmC, args, num_sms, stream)
-                     : launch_f4<false, false, true>(tmW, tmX, tmC, args, num_sms, stream);
-  }
+  // weights in TMEM (measured against smem-resident weights: square 8192^3 0.816 -> 0.700 ms,
+  // 16384^3 6.34 -> 5.49 ms, radio 1.600 -> 1.572 ms; the smem-weights instantiation was dropped)
   if (gemm_b1_f4_tma_words(args.Kw))
-    return tma_store ? launch_f4<true, true, false>(tmW, tmX, tmC, args, num_sms, stream)
-                     : launch_f4<false, true, false>(tmW, tmX, tmC, args, num_sms, stream);
-  return tma_store ? launch_f4<true, false, false>(tmW, tmX, tmC, args, num_sms, stream)
-                   : launch_f4<false, false, false>(tmW, tmX, tmC, args, num_sms, stream);
+    return tma_store ? launch_f4<true, true, true>(tmW, tmX, tmC, args, num_sms, stream)
+                     : launch_f4<false, true, true>(tmW, tmX, tmC, args, num_sms, stream);
+  return tma_store ? launch_f4<true, false, true>(tmW, tmX, tmC, args, num_sms, stream)
+                   : launch_f4<false, false, true>(tmW, tmX, tmC, args, num_sms, stream);
 }
 
 }  // namespace tcbf

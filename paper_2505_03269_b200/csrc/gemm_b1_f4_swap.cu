@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
             const uint64_t w_ri = smem_desc_k128(sWr, off);  // [W_r; W_i]
             const uint64_t w_nr = smem_desc_k128(sWn, off);  // [-W_i; W_r]
             const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (p.debug & 2) continue;
+            if (TCBF_ABLATE(p, 2)) continue;
             mma_mxf4(d, xr, w_ri, IDESC, sfa, sfb, acc);
             mma_mxf4(d, xi, w_nr, IDESC, sfa, sfb, 1u);
           }
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
         const int corr = part == 0 ? 0 : two_kpad;
 #pragma unroll
         for (int j = 0; j < 32; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
-        if (p.debug & 1) continue;
+        if (TCBF_ABLATE(p, 1)) continue;
         if constexpr (TMA_STORE) {  // box of 32 beams x 32 samples, row = beam (128 B)
           uint8_t* buf = bufs + sbuf * 4096;
           if (lane == 0) bulk_wait_group_read<1>();
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
         const uint4 i1 = *reinterpret_cast<const uint4*>(pr + plane + 16);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* st = smem + stage * C::STAGE_BYTES;
-        if (!(p.debug & 4)) {
+        if (!(TCBF_ABLATE(p, 4))) {
           if (x_side) {
             expand(st + row * 128, row, r0, r1);
             expand(st + C::X_TILE + row * 128, row, i0, i1);

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256, 2) cgemm_b1_mma_kernel(GemmB1Args p) {
           const int c0 = wn + j * 8 + g;
           const uint32_t br0 = sB[c0 * RS + w0], br1 = sB[c0 * RS + w0 + 4];
           const uint32_t bi0 = sB[(TN + c0) * RS + w0], bi1 = sB[(TN + c0) * RS + w0 + 4];
-          if (p.debug & 2) continue;
+          if (TCBF_ABLATE(p, 2)) continue;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             mma_b1_and(acc_re[i][j], ar[i], br0, br1);    // P(A_r & B_r)
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256, 2) cgemm_b1_mma_kernel(GemmB1Args p) {
             vr[e] = 4 * acc_re[i][j][2 * h + e] - 2 * (par + pai + pbr) + 2 * pbi;
             vi[e] = 4 * acc_im[i][j][2 * h + e] - 2 * (par + pai + pbr + pbi) + twoK;
           }
-          if (p.debug & 1) continue;
+          if (TCBF_ABLATE(p, 1)) continue;
           if ((p.N & 1) == 0 && n + 1 < p.N) {
             *reinterpret_cast<int2*>(ore + n) = make_int2(vr[0], vr[1]);
             *reinterpret_cast<int2*>(oim + n) = make_int2(vi[0], vi[1]);

@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 4);
-      mbar_init(&sfull_bar[s], EXPANDER_WARPS);
-      mbar_init(&sempty_bar[s], 4);
+      // every thread arrives after its own colsum accesses (no reliance on a warp-level
+      // sync before a single-lane arrive; keeps compute-sanitizer racecheck exact)
+      mbar_init(&sfull_bar[s], EXPANDER_WARPS * 32);
+      mbar_init(&sempty_bar[s], 4 * 32);
     }
     fence_barrier_init();
     if (TMA_STORE) tma_prefetch_desc(&tmC);
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t b_ri = smem_desc_k128(sBr, off);  // [B_r; B_i]
             const uint64_t b_cr = smem_desc_k128(sBc, off);  // [~B_i; B_r]
             const uint32_t acc = ((kb - kb0) | kk) ? 1u : 0u;
-            if (p.debug & 2) continue;
+            if (TCBF_ABLATE(p, 2)) continue;
             mma_i8_ss(d_re, ar, b_ri, IDESC, acc);  // [P(A_r & B_r) | P(A_r & B_i)]
             mma_i8_ss(d_re, ai, b_cr, IDESC, 1u);   // [P(A_i & ~B_i) | P(A_i & B_r)]
           }
@@ -221,13 +223,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int4 t4 = *reinterpret_cast<const int4*>(cterm + 4 * j);
           ct[4 * j] = t4.x; ct[4 * j + 1] = t4.y; ct[4 * j + 2] = t4.z; ct[4 * j + 3] = t4.w;
         }
-        if (ch == 2 * CHUNKS - 1) {  // last read of this tile's correction terms
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sempty_bar[cb]);
-        }
+        if (ch == 2 * CHUNKS - 1) mbar_arrive(&sempty_bar[cb]);  // last read of this tile's terms
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = (uint32_t)((int)v[j] + ct[j] + rterm);  // Re / Im, R1b
-        if (p.debug & 1) continue;
+        if (TCBF_ABLATE(p, 1)) continue;
         if constexpr (TMA_STORE) {
           if (lane == 0) bulk_wait_group_read<1>();
           __syncwarp();
@@ -329,7 +328,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         pc_i += __popc(wi.x) + __popc(wi.y) + __popc(wi.z) + __popc(wi.w);
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* st = smem + stage * STAGE_BYTES;
-        if (p.debug & 4) {
+        if (TCBF_ABLATE(p, 4)) {
         } else if (a_side) {
           uint8_t* ar = st + row * 128;
           uint8_t* ai = st + TILE_BYTES + row * 128;
@@ -362,8 +361,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int k_s = max(0, min(p.K, kb1 * 128) - kb0 * 128);
         colsum[(cb * 3 + 2) * 128 + row] = 2 * k_s - 2 * (pc_r + pc_i);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sfull_bar[cb]);
+      mbar_arrive(&sfull_bar[cb]);
       src_r = next_r;
       src_i = next_i;
       kb0 = nkb0;

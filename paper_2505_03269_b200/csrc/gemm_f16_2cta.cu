@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
   }
   tc_fence_before();
   cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
+  __syncthreads();  // (redundant with the cluster barrier; orders the alloc's smem write for racecheck)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
             const uint64_t ar = desc_a128(sAr, kk * 32), ai = desc_a128(sAi, kk * 32);
             const uint64_t br = desc_b_mn(sBr, kk * 16), bi = desc_b_mn(sBi, kk * 16);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (args.debug & 2) continue;
+            if (TCBF_ABLATE(args, 2)) continue;
             mma_f16_2sm(d_re, ar, br, IDESC, acc);
             mma_f16_2sm(d_re, ai, bi, IDESC_NEG, 1u);
             mma_f16_2sm(d_im, ar, bi, IDESC, acc);
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(tempty_leader[abuf]);
         }
-        if (args.debug & 1) continue;
+        if (TCBF_ABLATE(args, 1)) continue;
         const uint32_t* vv = v[ch & 1];
         if (lane == 0) bulk_wait_group_read<1>();
         __syncwarp();

@@ -39,17 +39,15 @@ constexpr int A_STAGE_BYTES = 2 * A_BYTES;
 constexpr int B_PLANE_BYTES = 2 * KMAX * 128;  // 2 column blocks x KMAX rows x 128 B
 constexpr int OFF_B = 0;
 constexpr int OFF_A = 2 * B_PLANE_BYTES;
-// Two epilogues: TMA stores staged through 32 KB of swizzled smem boxes (2 weight stages fit), or
-// DIRECT 256-bit st.global from registers (no staging), whose freed smem holds a third stage.
-template <bool DIRECT>
-struct FCfg {
-  static constexpr int A_STAGES = DIRECT ? 3 : 2;
-  static constexpr int EPI_BYTES = DIRECT ? 0 : EPI_WARPS * 2 * 4096;
-  static constexpr int OFF_EPI = OFF_A + A_STAGES * A_STAGE_BYTES;
-  static constexpr int BAR_OFFSET = OFF_EPI + EPI_BYTES;
-  static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
-  static_assert(SMEM_BYTES <= 232448, "smem budget");
-};
+// Epilogue: TMA stores staged through 32 KB of swizzled smem boxes, beside 2 weight stages.  (A
+// DIRECT variant -- 256-bit st.global from registers, a third weight stage in the freed smem -- was
+// bit-identical and measured 15% slower; dropped.)
+constexpr int A_STAGES = 2;
+constexpr int EPI_BYTES = EPI_WARPS * 2 * 4096;
+constexpr int OFF_EPI = OFF_A + A_STAGES * A_STAGE_BYTES;
+constexpr int BAR_OFFSET = OFF_EPI + EPI_BYTES;
+constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+static_assert(SMEM_BYTES <= 232448, "smem budget");
 
 __device__ __forceinline__ uint64_t desc_a128(const void* tile, uint32_t k_byte_off) {
   uint32_t addr = smem_u32(tile) + k_byte_off;
@@ -76,11 +74,15 @@ __device__ __forceinline__ uint64_t desc_b_res(const void* plane, uint32_t k_row
 // converters got bempty0 / converted block 0
 constexpr int TRACE_SLOTS = 1024;
 __device__ __forceinline__ void stamp(unsigned long long* tr, int slot) {
+#ifdef TCBF_DEV
   if (tr && slot < TRACE_SLOTS) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     tr[blockIdx.x * TRACE_SLOTS + slot] = t;
   }
+#else
+  (void)tr; (void)slot;
+#endif
 }
 
 __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
@@ -116,18 +118,16 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
 // MC: CTA pairs (clusters of 2) take adjacent units of the same batch entry, so their weight
 // tiles are identical: each CTA TMA-loads one of the two weight planes and multicasts it to both
 // (half the L2 -> SM weight traffic); both MMA issuers release a stage in both CTAs.
-template <int LAYOUT, bool VEC, bool MC, bool DIRECT>
+template <int LAYOUT, bool VEC, bool MC>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cgemm_f16_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                            GemmF16Args args, const float* __restrict__ xsrc, int K) {
-  using C = FCfg<DIRECT>;
-  constexpr int A_STAGES = C::A_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem + OFF_B;  // [2 planes][2 column blocks][KMAX rows][128 B]
   uint8_t* sA = smem + OFF_A;
-  uint8_t* epi_base = smem + C::OFF_EPI;
-  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + C::BAR_OFFSET);
+  uint8_t* epi_base = smem + OFF_EPI;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
   uint64_t* aempty = afull + A_STAGES;
   uint64_t* bfull = aempty + A_STAGES;    // [KMAX / BK]
   uint64_t* bempty = bfull + KMAX / BK;   // [KMAX / BK]
@@ -167,7 +167,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_relinquish();
   }
   tc_fence_before();
-  if (MC) cluster_sync(); else __syncthreads();  // peers signal this CTA's barriers
+  if (MC) cluster_sync();  // peers signal this CTA's barriers
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&aempty[stage], phase ^ 1);
             uint8_t* st = sA + stage * A_STAGE_BYTES;
-            if ((args.debug & 4) && mt > 0) {  // ablation: weight tiles loaded once per unit (wrong values)
+            if ((TCBF_ABLATE(args, 4)) && mt > 0) {  // ablation: weight tiles loaded once per unit (wrong values)
               mbar_arrive(&afull[stage]);
             } else {
               mbar_arrive_expect_tx(&afull[stage], A_STAGE_BYTES);
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t ar = desc_a128(st, kk * 32), ai = desc_a128(st + A_BYTES, kk * 32);
               const uint64_t br = desc_b_res(sB, krow), bi = desc_b_res(sB + B_PLANE_BYTES, krow);
               const uint32_t acc = (kb | kk) ? 1u : 0u;
-              if (args.debug & 2) continue;
+              if (TCBF_ABLATE(args, 2)) continue;
               mma_f16_ss(d_re, ar, br, IDESC, acc);
               mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);
               mma_f16_ss(d_im, ar, bi, IDESC, acc);
@@ -248,7 +249,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     constexpr int CHUNKS = BN / 32;
-    const bool vec8 = (args.N % 8 == 0) && ((reinterpret_cast<uintptr_t>(args.out) & 31) == 0);
     int sbuf = 0;
     int it = 0;
     for (int u = u_first; u < num_units; u += u_step) {
@@ -276,23 +276,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) mbar_arrive(&tempty[abuf]);
           }
           const uint32_t* vv = v[ch & 1];
-          if (args.debug & 1) continue;
-          if constexpr (DIRECT) {  // 256-bit stores straight from registers: thread = row, 128 B each
-            const int m = m0 + q * 32 + lane;
-            const int nb = n0 + c * 32;
-            if (m < args.M) {
-              float* row = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
-              if (vec8 && nb + 32 <= args.N) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  if (nb + j < args.N) row[j] = __uint_as_float(vv[j]);
-              }
-            }
-            continue;
-          }
+          if (TCBF_ABLATE(args, 1)) continue;
           // cooperative staging: the 4 epilogue warps fill one 128-row x 32-column box (16 KB),
           // one thread issues a single TMA store per chunk
           uint8_t* buf = epi_base + sbuf * 16384;
@@ -316,7 +300,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (threadIdx.x == 64) stamp(args.trace, 4 * it + 3);
       }
     }
-    if (!DIRECT && threadIdx.x == 64) bulk_wait_group<0>();
+    if (threadIdx.x == 64) bulk_wait_group<0>();
   } else {
     // ------------------------------------------------------------ converters: fp32 data -> resident B
     const int ct = threadIdx.x - (2 + EPI_WARPS) * 32;  // 0..255
@@ -388,11 +372,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <int LAYOUT, bool VEC, bool MC, bool DIRECT>
+template <int LAYOUT, bool VEC, bool MC>
 cudaError_t launch_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& a, const float* x,
                          int K, int num_sms, cudaStream_t s) {
-  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC, MC, DIRECT>;
-  constexpr int SMEM_BYTES = FCfg<DIRECT>::SMEM_BYTES;
+  auto kern = cgemm_f16_fused_kernel<LAYOUT, VEC, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = a.B * a.tiles_n;
@@ -421,17 +404,11 @@ cudaError_t launch_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const G
 
 template <int LAYOUT, bool VEC>
 cudaError_t launch_fused_sel(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& a, const float* x,
-                             int K, int num_sms, cudaStream_t s) {
+                             int K, bool multicast, int num_sms, cudaStream_t s) {
   // weight multicast across CTA pairs needs pairs of units of one batch entry (tiles_n even)
-  const char* env = getenv("TCBF_F16_MC");
-  const bool mc = a.tiles_n % 2 == 0 && a.B * a.tiles_n >= 2 && !(env && atoi(env) == 0);
-  const char* denv = getenv("TCBF_F16_DIRECT");
-  const bool direct = denv && atoi(denv) != 0;
-  if (direct)
-    return mc ? launch_fused<LAYOUT, VEC, true, true>(tmA, tmC, a, x, K, num_sms, s)
-              : launch_fused<LAYOUT, VEC, false, true>(tmA, tmC, a, x, K, num_sms, s);
-  return mc ? launch_fused<LAYOUT, VEC, true, false>(tmA, tmC, a, x, K, num_sms, s)
-            : launch_fused<LAYOUT, VEC, false, false>(tmA, tmC, a, x, K, num_sms, s);
+  const bool mc = multicast && a.tiles_n % 2 == 0 && a.B * a.tiles_n >= 2;
+  return mc ? launch_fused<LAYOUT, VEC, true>(tmA, tmC, a, x, K, num_sms, s)
+            : launch_fused<LAYOUT, VEC, false>(tmA, tmC, a, x, K, num_sms, s);
 }
 
 }  // namespace
@@ -439,12 +416,13 @@ cudaError_t launch_fused_sel(const CUtensorMap& tmA, const CUtensorMap& tmC, con
 bool gemm_f16_fused_supported(int64_t K16, int64_t N) { return K16 <= KMAX && N % 4 == 0; }
 
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
-                                  const float* x_src, int layout, int K, int num_sms, cudaStream_t stream) {
+                                  const float* x_src, int layout, int K, bool multicast, int num_sms,
+                                  cudaStream_t stream) {
   const bool vec = layout == 0 && (args.N % 8 == 0) && (reinterpret_cast<uintptr_t>(x_src) % 16 == 0);
   if (layout == 0)
-    return vec ? launch_fused_sel<0, true>(tmA, tmC, args, x_src, K, num_sms, stream)
-               : launch_fused_sel<0, false>(tmA, tmC, args, x_src, K, num_sms, stream);
-  return launch_fused_sel<1, false>(tmA, tmC, args, x_src, K, num_sms, stream);
+    return vec ? launch_fused_sel<0, true>(tmA, tmC, args, x_src, K, multicast, num_sms, stream)
+               : launch_fused_sel<0, false>(tmA, tmC, args, x_src, K, multicast, num_sms, stream);
+  return launch_fused_sel<1, false>(tmA, tmC, args, x_src, K, multicast, num_sms, stream);
 }
 
 }  // namespace tcbf

@@ -37,13 +37,11 @@ struct F16Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int EPI_BUFS = 2;
-  // EPI: 0 = swizzled smem staging + TMA bulk store, 1 = direct 256-bit st.global from
-  // registers (no smem traffic; needs N % 8 == 0), 2 = masked scalar stores (any N),
-  // 3 = swizzled smem staging + coalesced 128-bit st.global (4 full lines per warp store,
-  //     keeps the per-SM TMA engine free for the operand loads; needs N % 4 == 0)
-  //     4 = cooperative staging: the 4 epilogue warps fill one 128-row x 32-column box (16 KB)
-  //         and one thread issues a single TMA store per chunk (4x fewer bulk operations)
-  static constexpr int EPI_BYTES = (EPI == 0 || EPI == 3 || EPI == 4) ? EPI_WARPS * EPI_BUFS * 4096 : 0;
+  // EPI: 0 = swizzled smem staging + TMA bulk store (N % 4 == 0), 2 = masked scalar stores (any N).
+  // (Measured and dropped: direct 256-bit st.global from registers, smem-staged coalesced
+  // st.global, cooperative 128-row TMA boxes -- all slower than EPI 0.)
+  static_assert(EPI == 0 || EPI == 2, "epilogue kind");
+  static constexpr int EPI_BYTES = EPI == 0 ? EPI_WARPS * EPI_BUFS * 4096 : 0;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x (D_r, D_i)
   static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
             const uint64_t ar = desc_a<BK>(sAr, kk * 32), ai = desc_a<BK>(sAi, kk * 32);
             const uint64_t br = desc_b_mn<BK>(sBr, kk * 16), bi = desc_b_mn<BK>(sBi, kk * 16);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (args.debug & 2) continue;
+            if (TCBF_ABLATE(args, 2)) continue;
             mma_f16_ss(d_re, ar, br, IDESC, acc);     // Re += Re(a) Re(b)
             mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);  // Re += -Im(a) Im(b)
             mma_f16_ss(d_im, ar, bi, IDESC, acc);     // Im += Re(a) Im(b)
@@ -227,28 +225,8 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
           if (lane == 0) mbar_arrive(&tempty_bar[abuf]);
         }
         const uint32_t* vv = v[i & 1];
-        if (args.debug & 1) continue;
-        if constexpr (EPI == 4) {
-          static_assert(EPI_WARPS == 4, "cooperative epilogue uses exactly 4 warps");
-          // buffer sbuf: 128 rows x 128 B; warp q owns rows 32q..32q+31 (the TMEM quadrant)
-          uint8_t* buf = epi_base + sbuf * 16384;
-          if (threadIdx.x == 64) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();  // issuing thread (warp 2)
-          asm volatile("bar.sync 1, 128;" ::: "memory");                  // buffer free for everyone
-          const int row = q * 32 + lane;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int pos = j ^ (row & 7);
-            *reinterpret_cast<uint4*>(buf + row * 128 + pos * 16) =
-                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
-          }
-          fence_proxy_async_smem();
-          asm volatile("bar.sync 1, 128;" ::: "memory");                  // box complete
-          if (threadIdx.x == 64) {
-            tma_store_3d(&tmC, buf, n0 + c * 32, m0, 2 * b + part);
-            bulk_commit_group();
-          }
-          sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
-        } else if constexpr (EPI == 0) {
+        if (TCBF_ABLATE(args, 1)) continue;
+        if constexpr (EPI == 0) {
           if (lane == 0) bulk_wait_group_read<Cfg::EPI_BUFS - 1>();
           __syncwarp();
           uint8_t* buf = stg + sbuf * 4096;
@@ -265,43 +243,6 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
             bulk_commit_group();
           }
           sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
-        } else if constexpr (EPI == 3) {
-          uint8_t* buf = stg + sbuf * 4096;
-          __syncwarp();  // previous readers of this buffer are done
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int pos = j ^ (lane & 7);
-            *reinterpret_cast<uint4*>(buf + lane * 128 + pos * 16) =
-                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
-          }
-          __syncwarp();
-          const int rsub = lane >> 3, cj = lane & 7;  // 4 rows x 8 16-byte chunks per instruction
-          const int nb = n0 + c * 32 + cj * 4;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rr = i * 4 + rsub;
-            const uint4 val = *reinterpret_cast<const uint4*>(buf + rr * 128 + ((cj ^ (rr & 7)) << 4));
-            const int m = m0 + q * 32 + rr;
-            if (m < args.M && nb < args.N) {
-              float* dst = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
-              __stcs(reinterpret_cast<uint4*>(dst), val);  // streaming: written once, never re-read here
-            }
-          }
-          sbuf = (sbuf + 1 == Cfg::EPI_BUFS) ? 0 : sbuf + 1;
-        } else if constexpr (EPI == 1) {
-          const int m = m0 + q * 32 + lane;
-          const int nb = n0 + c * 32;
-          if (m < args.M) {
-            float* row = args.out + ((size_t)(2 * b + part) * args.M + m) * (size_t)args.N + nb;
-            if (nb + 32 <= args.N) {
-#pragma unroll
-              for (int j = 0; j < 4; ++j) st_global_v8(row + 8 * j, vv + 8 * j);
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (nb + j < args.N) row[j] = __uint_as_float(vv[j]);
-            }
-          }
         } else {
           const int m = m0 + q * 32 + lane;
           if (m < args.M) {
@@ -314,9 +255,6 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
           }
         }
       }
-    }
-    if constexpr (EPI == 4) {
-      if (threadIdx.x == 64) bulk_wait_group<0>();
     }
     if constexpr (EPI == 0) {
       if (lane == 0) bulk_wait_group<0>();
@@ -352,15 +290,7 @@ cudaError_t dispatch(int variant, int epi, const CUtensorMap& a, const CUtensorM
   }
   switch (variant) {
     case F16_V_N64:       return launch_impl<64, 64, 4, 4, 0>(a, b, c, g, sms, s);
-    case F16_V_K64_S3:    return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
     case F16_V_K32_S4_E8: return launch_impl<128, 32, 4, 8, 0>(a, b, c, g, sms, s);
-    case F16_V_K64_S2_E8: return launch_impl<128, 64, 2, 8, 0>(a, b, c, g, sms, s);
-    case F16_V_K32_S6_E4: return launch_impl<128, 32, 6, 4, 0>(a, b, c, g, sms, s);
-    case F16_V_K64_S3_DIRECT: return launch_impl<128, 64, 3, 4, 1>(a, b, c, g, sms, s);
-    case F16_V_K64_S3_DIRECT_E8: return launch_impl<128, 64, 3, 8, 1>(a, b, c, g, sms, s);
-    case F16_V_K64_S3_STG: return launch_impl<128, 64, 3, 4, 3>(a, b, c, g, sms, s);
-    case F16_V_K64_S3_STG_E8: return launch_impl<128, 64, 2, 8, 3>(a, b, c, g, sms, s);
-    case F16_V_K64_S3_COOP: return launch_impl<128, 64, 3, 4, 4>(a, b, c, g, sms, s);
     default:              return launch_impl<128, 64, 3, 4, 0>(a, b, c, g, sms, s);
   }
 }
@@ -378,7 +308,7 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
 }
 
 int gemm_f16_block_k(int variant) {
-  return (variant == F16_V_K32_S4_E8 || variant == F16_V_K32_S6_E4) ? 32 : 64;
+  return variant == F16_V_K32_S4_E8 ? 32 : 64;
 }
 
 }  // namespace tcbf

@@ -6,32 +6,34 @@
 
 namespace tcbf {
 
+// Ablation switches of the measurement studies in DESIGN.md §4 (skip stores / MMAs / expansion).
+// They exist only in TCBF_DEV builds (TCBF_DEBUG env, read once at plan creation); the product
+// library compiles them out, so its results never depend on the environment at call time.
+#ifdef TCBF_DEV
+#define TCBF_ABLATE(args, bit) (((args).debug & (bit)) != 0)
+#else
+#define TCBF_ABLATE(args, bit) false
+#endif
+
 struct GemmF16Args {
   int M, N, B;
   int K16;
   int tiles_m, tiles_n, num_tiles, num_kb;
   float* out;  // used by the masked-store epilogue (N % 4 != 0)
-  int debug;   // ablation (TCBF_DEBUG): bit0 skip output stores, bit1 skip MMAs
+  int debug;   // TCBF_DEV ablation: bit0 skip output stores, bit1 skip MMAs
   int group_m; // tile rows per rasterisation group (tile_coords)
   int splits, kb_per_split;  // K split of the streaming-conversion kernel (fp32 TMA reduce-add)
-  unsigned long long* trace;  // dev timeline (TCBF_TRACE=<file>, fused kernel): globaltimer stamps
+  unsigned long long* trace;  // TCBF_DEV timeline of the fused kernel (globaltimer stamps), else null
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
 enum {
-  F16_V_K32_S4_E8 = 0,  // 128x128, BK 32, 4 stages, 8 epilogue warps (default)
-  F16_V_K64_S3 = 1,     // 128x128, BK 64, 3 stages, 4 epilogue warps
-  F16_V_K64_S2_E8 = 2,  // 128x128, BK 64, 2 stages, 8 epilogue warps
-  F16_V_K32_S6_E4 = 3,  // 128x128, BK 32, 6 stages, 4 epilogue warps
-  F16_V_N64 = 4,        // 128x64,  BK 64, 4 stages, 4 epilogue warps (small N)
-  F16_V_K64_S3_DIRECT = 5,     // 128x128, BK 64, 3 stages, 4 epilogue warps, direct 256-bit stores
-  F16_V_K64_S3_DIRECT_E8 = 6,  // same with 8 epilogue warps
-  F16_V_2CTA_N128 = 7,  // CTA pair, 256x128 tile, BK 64, 4 stages, double-buffered TMEM
-  F16_V_2CTA_N256 = 8,  // CTA pair, 256x256 tile, BK 64, 3 stages, single TMEM buffer
-  F16_V_K64_S3_STG = 9,     // 128x128, BK 64, 3 stages, smem-staged coalesced st.global epilogue
-  F16_V_K64_S3_STG_E8 = 10, // same, 2 stages, 8 epilogue warps
-  F16_V_K64_S3_COOP = 11,   // 128x128, BK 64, 3 stages, cooperative 128-row TMA-store boxes
-  F16_V_COUNT = 12
+  F16_V_K32_S4_E8 = 0,  // 128x128, BK 32, 4 stages, 8 epilogue warps
+  F16_V_K64_S3 = 1,     // 128x128, BK 64, 3 stages, 4 epilogue warps (default 1-CTA tile)
+  F16_V_N64 = 2,        // 128x64,  BK 64, 4 stages, 4 epilogue warps (small N)
+  F16_V_2CTA_N128 = 3,  // CTA pair, 256x128 tile, BK 64, 4 stages, double-buffered TMEM
+  F16_V_2CTA_N256 = 4,  // CTA pair, 256x256 tile, BK 64, 3 stages, single TMEM buffer
+  F16_V_COUNT = 5
 };
 int gemm_f16_block_n(int variant);
 cudaError_t launch_gemm_f16_2cta(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
@@ -50,26 +52,22 @@ int gemm_f16_conv_block_k();
 int gemm_f16_conv_splits(int tiles, int num_kb, int num_sms);
 cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                  const GemmF16Args& args, int layout, int num_sms, cudaStream_t stream);
-cudaError_t launch_gemm_f16_fused2(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
-                                   const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
-                                  const float* x_src, int layout, int K, int num_sms, cudaStream_t stream);
+                                  const float* x_src, int layout, int K, bool multicast, int num_sms,
+                                  cudaStream_t stream);
 
 struct GemmB1Args {
   const uint32_t* w;  // [B][2][M][Kw]
   const uint32_t* x;  // [B][2][N][Kw]
   int32_t* out;       // [B][2][M][N]
   int M, N, K, Kw, B;
-  int debug;  // ablation (TCBF_DEBUG): bit0 skip stores, bit1 skip MMAs, bit2 skip expansion
+  int debug;  // TCBF_DEV ablation: bit0 skip stores, bit1 skip MMAs, bit2 skip expansion
   int group_m;  // tile rows per rasterisation group (tile_coords)
   int splits;   // split-K factor (int8 kernel): >1 accumulates exact int32 partials with TMA reduce-add
   int kb_per_split;
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_mma(const GemmB1Args& args, cudaStream_t stream);  // legacy mma.sync b1 AND
-cudaError_t launch_gemm_b1_2cta(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
-                                cudaStream_t stream);
-bool gemm_b1_f8_supported(int64_t Kw);
 bool gemm_b1_f4_supported(int64_t Kw);
 int gemm_b1_f4_block_words();
 bool gemm_b1_f4_tma_words(int64_t Kw);
@@ -77,15 +75,8 @@ int gemm_b1_f4_store_box_cols(int64_t Kw);
 int gemm_b1_f4_swap_beams(int64_t M);  // beams per tile of the swapped small-M kernel (0: not used)
 cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                    const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
-cudaError_t launch_gemm_b1_f4_2cta(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
-                                   cudaStream_t stream);
 cudaError_t launch_gemm_b1_f4(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                               const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
-bool gemm_b1_fused_supported(int64_t Kw, int64_t N);
-cudaError_t launch_gemm_b1_fused(const CUtensorMap& tmC, const GemmB1Args& args, const float* x_src, int layout,
-                                 int num_sms, cudaStream_t stream);
-cudaError_t launch_gemm_b1_f8(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
-                              cudaStream_t stream);
 cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,
                               cudaStream_t stream);
 
@@ -96,7 +87,8 @@ cudaError_t launch_steering(const double* pos, const double* theta, const double
 // pack kernels (pack.cu)
 cudaError_t launch_pack_f16(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
                             int64_t K16, uint16_t* dst, cudaStream_t stream);
+// wpt: 1-bit data pack words per thread (32, 8, 2, 1), 0 = chosen by operand size
 cudaError_t launch_pack_b1(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
-                           int64_t Kw, uint32_t* dst, cudaStream_t stream);
+                           int64_t Kw, int wpt, uint32_t* dst, cudaStream_t stream);
 
 }  // namespace tcbf

@@ -4,12 +4,14 @@
 // matrices are tiled in device memory ... a transpose kernel"; real and
 // imaginary components separated).
 //
-//   F16: fp32 -> fp16 round-to-nearest-even (cvt.rn.f16.f32), planar, K-contiguous,
-//        K padded with zeros to Kp = round_up(K, 64) (one 128-byte swizzle row).
+//   F16: fp32 -> fp16 round-to-nearest-even (cvt.rn.f16.f32), planar.  Weights [B][M][K] ->
+//        [B][2][M][Kp], K-contiguous, K padded with zeros to Kp = round_up(K, 64) (one 128-byte
+//        swizzle row).  Data [B][K][N] -> [B][2][K][Np], N-contiguous, Np = round_up(N, 8):
+//        NO transpose -- the GEMMs read the data MN-major (the tcgen05 B-major descriptor bit).
 //   B1 : bit = (value >= 0) (reading R4), LSB-first along K, padding
 //        bits 0, Kp = round_up(ceil(K/32), 8) words (256-bit granule).
-// Weights [B][M][K] keep their row order; data [B][K][N] is transposed to [B][2][N][Kp]
-// so both GEMM operands are K-major (what the tcgen05 smem descriptors and TMA want).
+//        Weights keep their row order [B][2][M][Kp]; data [B][K][N] is transposed to
+//        [B][2][N][Kp] so the bits of one sample run along K (the paper's transpose kernel).
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -170,7 +172,7 @@ cudaError_t launch_pack_f16(const float* src, int layout, int operand, int64_t B
 }
 
 cudaError_t launch_pack_b1(const float* src, int layout, int operand, int64_t B, int64_t R, int64_t C,
-                           int64_t Kw, uint32_t* dst, cudaStream_t stream) {
+                           int64_t Kw, int wpt_override, uint32_t* dst, cudaStream_t stream) {
   if (operand == 0) {
     const int64_t work = B * R * Kw * 32;
     if (layout == 0) pack_b1_rows<0><<<grid_for(work, 256), 256, 0, stream>>>(src, B, R, C, Kw, dst);
@@ -181,7 +183,7 @@ cudaError_t launch_pack_b1(const float* src, int layout, int operand, int64_t B,
     // 41.7 -> 10.6, M=32 N=K=4096 52.6 -> 41, N=K=16384 385 -> 345, radio 1-bit unchanged (644)
     int wpt = 32;
     while (wpt > 1 && B * C * ((Kw + wpt - 1) / wpt) < 4LL * 148 * 2048) wpt = wpt == 32 ? 8 : wpt == 8 ? 2 : 1;
-    if (const char* env = getenv("TCBF_PACK_WPT")) wpt = atoi(env);  // experiments: 32, 8, 2 or 1
+    if (wpt_override > 0) wpt = wpt_override;  // experiments / tests: 32, 8, 2 or 1
     wpt = wpt >= 32 ? 32 : wpt >= 8 ? 8 : wpt >= 2 ? 2 : 1;
     dim3 grid((unsigned)((C + 127) / 128), (unsigned)cap_dim((Kw + wpt - 1) / wpt), (unsigned)cap_dim(B));
 #define TCBF_PACK_B1_T(L, W) pack_b1_transpose<L, W><<<grid, 128, 0, stream>>>(src, B, R, C, Kw, dst)

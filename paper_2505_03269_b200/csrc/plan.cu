@@ -121,11 +121,249 @@ void retain_pool_memory() {
   }
 }
 
+void tcbf_internal_set_launches(int n) { g_launches = n; }
+
+tcbf_status tcbf_internal_fail(tcbf_status s, const char* what) { return fail(s, "%s", what); }
+
+tcbf_status tcbf_internal_cuda_fail(cudaError_t e, const char* what) { return cuda_fail(e, what); }
+
 namespace {
+
+// Experiment overrides (DESIGN.md §4 variant studies, tests that force a kernel).  Read ONCE, at
+// plan creation; a plan never consults the environment again, so its results and its kernel
+// choice are fixed for its lifetime (the immutable plan of SURVEY.md §8b).
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+bool env_set(const char* name) { return getenv(name) != nullptr; }
+
+// Streaming-conversion kernel units (column tiles x K splits) for an M <= 128 fp16 plan.
+int64_t conv_units(const tcbf_plan* p, int* splits) {
+  const int64_t tiles = ((p->N + 127) / 128) * p->B;
+  const int bk = tcbf::gemm_f16_conv_block_k();
+  const int nkb = (int)((p->K + bk - 1) / bk);
+  int sp = tiles < INT32_MAX ? tcbf::gemm_f16_conv_splits((int)tiles, nkb, p->num_sms) : 1;
+  if (p->conv_splits_override > 0) sp = std::max(1, std::min(p->conv_splits_override, nkb));
+  const int kbps = (nkb + sp - 1) / sp;
+  sp = (nkb + kbps - 1) / kbps;
+  if (splits) *splits = sp;
+  return tiles * sp;
+}
+
+void choose_kernels(tcbf_plan* p) {
+  // fp16 GEMM tile: 128x64 when N <= 64, else 128x128 (BK 64, 3 stages, 4 epilogue warps); CTA
+  // pairs (cta_group::2) halve the per-SM shared-memory traffic of the B operand when M spans more
+  // than one 128-row tile and K is long enough to be compute-bound (DESIGN.md §4 variant table)
+  if (p->N <= 64) p->f16_variant = tcbf::F16_V_N64;
+  else if (p->M <= 128 || p->N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
+  else if (p->K >= 2048 && p->N >= 256) p->f16_variant = tcbf::F16_V_2CTA_N256;  // long K: compute-bound
+  else if (p->kp > 256) p->f16_variant = tcbf::F16_V_2CTA_N128;                 // mid K (measured +5-8%)
+  else p->f16_variant = tcbf::F16_V_K64_S3;                                       // short K: store-bound
+  const int v = env_int("TCBF_F16_VARIANT", -1);
+  if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
+
+  // 1-bit: +-1 fp4 (kind::mxf4) tensor cores, exact while 32 Kw <= 2^23; int8 AND form beyond
+  p->b1_kernel = tcbf::gemm_b1_f4_supported(p->kp) ? TCBF_B1K_F4 : TCBF_B1K_I8;
+  if (const char* e = getenv("TCBF_B1_KERNEL")) {
+    if (strcmp(e, "popc") == 0) p->b1_kernel = TCBF_B1K_POPC;
+    else if (strcmp(e, "i8") == 0) p->b1_kernel = TCBF_B1K_I8;
+    else if (strcmp(e, "bmma") == 0) p->b1_kernel = TCBF_B1K_BMMA;
+    else if (strcmp(e, "f4") == 0 && tcbf::gemm_b1_f4_supported(p->kp)) p->b1_kernel = TCBF_B1K_F4;
+  }
+  p->b1_swap_beams = (p->b1_kernel == TCBF_B1K_F4 && !env_set("TCBF_NO_SWAP")) ? tcbf::gemm_b1_f4_swap_beams(p->M) : 0;
+  // split-K of the int8 kernel: measured not to shorten the per-SM K chain, so only forced (tests)
+  p->b1_splits = 1;
+  p->b1_kb_per_split = (int)(p->kp / 4);
+  if (p->b1_kernel == TCBF_B1K_I8) {
+    const int64_t nkb = p->kp / 4;
+    const int64_t sp = std::min<int64_t>(std::max(1, env_int("TCBF_B1_SPLITS", 1)), nkb);
+    if (sp > 1) {
+      p->b1_kb_per_split = (int)((nkb + sp - 1) / sp);
+      p->b1_splits = (int)((nkb + p->b1_kb_per_split - 1) / p->b1_kb_per_split);
+    }
+  }
+  p->pack_wpt = env_int("TCBF_PACK_WPT", 0);
+
+  // tcbf_beamform_raw: data conversion fused into the GEMM where the shape allows it
+  const bool no_fused = env_int("TCBF_NO_FUSED", 0) != 0;
+  p->f16_multicast = env_int("TCBF_F16_MC", 1) != 0;
+  p->conv_splits_override = env_int("TCBF_CONV_SPLITS", 0);
+  p->raw_mode = TCBF_RAW_PACK;
+  if (p->prec == TCBF_PREC_F16 && !no_fused) {
+    if (tcbf::gemm_f16_fused_supported(p->kp, p->N)) {
+      p->raw_mode = TCBF_RAW_FUSED;
+    } else if (p->M <= 128 && p->N % 4 == 0) {
+      // every data element enters one tile: stream the fp32 data through the GEMM once; needs
+      // enough (column tile x K split) units to occupy the GPU (measured: below a quarter of
+      // the SMs, pack + GEMM wins)
+      if (conv_units(p, nullptr) >= p->num_sms / 4 || env_set("TCBF_FORCE_STREAM_CONV")) p->raw_mode = TCBF_RAW_STREAM;
+    }
+  }
+  p->debug = 0;
+#ifdef TCBF_DEV
+  p->debug = env_int("TCBF_DEBUG", 0);
+#endif
+}
+
+const char* gemm_kernel_name(const tcbf_plan* plan) {
+  if (plan->prec == TCBF_PREC_B1) {
+    const bool tma = plan->N % 4 == 0;
+    switch (plan->b1_kernel) {
+      case TCBF_B1K_POPC: return "b1_popc_xor_64x64";
+      case TCBF_B1K_BMMA: return "b1_mma_sync_and_128x64";
+      case TCBF_B1K_I8: return tma ? "b1_tcgen05_i8_128x128_tma" : "b1_tcgen05_i8_128x128_stg";
+      default: break;
+    }
+    if (plan->b1_swap_beams == 32)
+      return tma ? "b1_tcgen05_mxf4pm1_swap_128x32_tma" : "b1_tcgen05_mxf4pm1_swap_128x32_stg";
+    if (plan->b1_swap_beams == 64)
+      return tma ? "b1_tcgen05_mxf4pm1_swap_128x64_tma" : "b1_tcgen05_mxf4pm1_swap_128x64_stg";
+    return tma ? "b1_tcgen05_mxf4pm1_atmem_128x128_tma" : "b1_tcgen05_mxf4pm1_atmem_128x128_stg";
+  }
+  if (plan->N % 4 != 0)
+    return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked" : "f16_tcgen05_128x128_masked";
+  static const char* names[tcbf::F16_V_COUNT] = {
+      "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x64_k64s4e4_tma",
+      "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma"};
+  return names[plan->f16_variant];
+}
 
 }  // namespace
 
-void tcbf_internal_set_launches(int n) { g_launches = n; }
+namespace {
+
+tcbf_status beamform_f16(const tcbf_plan* plan, const void* w_packed, const void* x_packed, void* out,
+                         cudaStream_t st) {
+  // Final kernel choice first, so the tensor-map boxes always match the instantiation:
+  // TMA bulk store needs N % 4 == 0 (16-B row stride), otherwise the masked-store epilogue
+  // (instantiated for the N64 and K64_S3 tiles only).
+  int var = plan->f16_variant;
+  int epi = 0;
+  if (plan->N % 4 != 0) {
+    epi = 2;
+    if (var != tcbf::F16_V_N64) var = tcbf::F16_V_K64_S3;
+  }
+  const int bn = tcbf::gemm_f16_block_n(var);
+  const int bk = tcbf::gemm_f16_block_k(var);
+  const bool use_pair = var == tcbf::F16_V_2CTA_N128 || var == tcbf::F16_V_2CTA_N256;
+  CUtensorMap ta, tb, tc;
+  // A (weights, K-major [2B][M][K16]): box {BK, 128}, swizzle = BK * 2 bytes
+  tcbf_status s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk,
+                            128, bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (s != TCBF_OK) return s;
+  // B (data, MN-major [2B][K][Np]): box {64 columns, BK rows}, 128-byte swizzle; K tail is OOB -> 0
+  s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->n_packed, plan->K, 2 * plan->B, 64, bk,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  if (s != TCBF_OK) return s;
+  if (epi == 0) {
+    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+    if (s != TCBF_OK) return s;
+  } else {
+    memset(&tc, 0, sizeof(tc));
+  }
+  tcbf::GemmF16Args a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+  a.tiles_m = (int)((plan->M + (use_pair ? 255 : 127)) / (use_pair ? 256 : 128));
+  a.tiles_n = (int)((plan->N + bn - 1) / bn);
+  const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
+  if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+  a.num_tiles = (int)nt;
+  a.num_kb = (int)(plan->kp / bk);
+  a.out = static_cast<float*>(out);
+  {  // rasterisation group: keep ~48 MB of weight rows (A_r + A_i, K16 fp16) of a group in L2
+    const int64_t rows_per_tile = use_pair ? 256 : 128;
+    const int64_t bytes_per_tile_row = rows_per_tile * plan->kp * 4;
+    int64_t gm = (48ll << 20) / (bytes_per_tile_row > 0 ? bytes_per_tile_row : 1);
+    a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, a.tiles_m));
+  }
+  a.debug = plan->debug;
+  cudaError_t e = use_pair ? tcbf::launch_gemm_f16_2cta(ta, tb, tc, a, bn, plan->num_sms, st)
+                           : tcbf::launch_gemm_f16(ta, tb, tc, a, var, epi, plan->num_sms, st);
+  if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
+  g_launches = 1;
+  return TCBF_OK;
+}
+
+tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void* x_packed, void* out,
+                        cudaStream_t st) {
+  tcbf::GemmB1Args a;
+  memset(&a, 0, sizeof(a));
+  a.w = static_cast<const uint32_t*>(w_packed);
+  a.x = static_cast<const uint32_t*>(x_packed);
+  a.out = static_cast<int32_t*>(out);
+  a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
+  a.debug = plan->debug;
+  {  // rasterisation group: 1-bit operands are small; ~16 MB of packed weight rows per group
+    const int64_t bytes_per_tile_row = 128 * plan->kp * 8;
+    const int64_t tm = (plan->M + 127) / 128;
+    a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bytes_per_tile_row, tm));
+  }
+  a.splits = plan->b1_splits;
+  a.kb_per_split = plan->b1_kb_per_split;
+  cudaError_t e;
+  if (a.splits > 1) {  // exact int32 partials reduce-added into a zeroed output
+    e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
+  }
+  const bool tma_store = (plan->N % 4) == 0;
+  tcbf_status s;
+  if (plan->b1_kernel == TCBF_B1K_BMMA) {
+    e = tcbf::launch_gemm_b1_mma(a, st);
+  } else if (plan->b1_kernel == TCBF_B1K_POPC) {
+    e = tcbf::launch_gemm_b1_popc(a, st);
+  } else {
+    CUtensorMap tc;
+    memset(&tc, 0, sizeof(tc));
+    if (plan->b1_swap_beams) {  // few beams: samples on the 128-row MMA dimension, beams on N
+      CUtensorMap tw, tx;
+      const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
+      s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw,
+                    (uint32_t)plan->b1_swap_beams, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      if (s != TCBF_OK) return s;
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      if (s != TCBF_OK) return s;
+      if (tma_store) {  // 32 beams x 32 samples boxes, unswizzled 128-byte rows
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (s != TCBF_OK) return s;
+      }
+      e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, tma_store, plan->num_sms, st);
+    } else if (plan->b1_kernel == TCBF_B1K_F4) {  // packed words by TMA: box {one 256-bit K block, 128 rows}
+      CUtensorMap tw, tx;
+      if (tma_store) {
+        const bool box16 = tcbf::gemm_b1_f4_store_box_cols(plan->kp) == 16;  // 32 x 16 boxes, 64-byte swizzle
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, box16 ? 16 : 32, 32,
+                      box16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (s != TCBF_OK) return s;
+      }
+      const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
+      s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw, 128,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      if (s != TCBF_OK) return s;
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      if (s != TCBF_OK) return s;
+      e = tcbf::launch_gemm_b1_f4(tw, tx, tc, a, tma_store, plan->num_sms, st);
+    } else {  // int8 AND form: per-warp 32-row x 32-column boxes
+      if (tma_store) {
+        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
+        if (s != TCBF_OK) return s;
+      }
+      e = tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
+  g_launches = a.splits > 1 ? 2 : 1;  // memset + kernel when split-K
+  return TCBF_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -159,6 +397,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
                 minor);
   tcbf_plan* p = new (std::nothrow) tcbf_plan_s;
   if (!p) return fail(TCBF_ERR_ALLOC, "host allocation of the plan failed");
+  memset(p, 0, sizeof(*p));
   p->M = M; p->N = N; p->K = K; p->B = batch;
   p->prec = precision;
   p->kp = kp;
@@ -166,30 +405,7 @@ tcbf_status tcbf_plan_create(tcbf_plan** plan, int64_t M, int64_t N, int64_t K, 
   p->num_sms = sms;
   p->w_bytes = wb; p->x_bytes = xb; p->out_bytes = ob;
   p->n_packed = (N + 7) / 8 * 8;
-  // fp16 kernel variant: 128x64 tiles when N <= 64, else 128x128 (BK 32, 4 stages, 8 epilogue warps)
-  // CTA pairs (cta_group::2) halve the per-SM shared-memory traffic of the B operand; used when
-  // M spans more than one 128-row tile.  256-wide tiles when K is long (compute-bound shapes).
-  if (N <= 64) p->f16_variant = tcbf::F16_V_N64;
-  else if (M <= 128 || N % 4 != 0) p->f16_variant = tcbf::F16_V_K64_S3;
-  else if (K >= 2048 && N >= 256) p->f16_variant = tcbf::F16_V_2CTA_N256;   // long K: compute-bound
-  else if (kp > 256) p->f16_variant = tcbf::F16_V_2CTA_N128;              // mid K (measured +5-8%)
-  else p->f16_variant = tcbf::F16_V_K64_S3;                               // short K: store-bound
-  if (const char* env = getenv("TCBF_F16_VARIANT")) {
-    int v = atoi(env);
-    if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
-  }
-  // +-1 fp4 (kind::mxf4) kernel by default: measured 1.3-1.4x faster than the int8 AND-form
-  // kernel (radio 2.19 -> 1.71 ms, square 8192^3 1.62 -> 1.13 ms); int8 beyond its exact range
-  p->b1_tc = tcbf::gemm_b1_f4_supported(kp) ? 4 : 1;
-  if (const char* env = getenv("TCBF_B1_KERNEL")) {
-    if (strcmp(env, "popc") == 0) p->b1_tc = 0;
-    else if (strcmp(env, "i8") == 0) p->b1_tc = 1;
-    else if (strcmp(env, "f8") == 0 && tcbf::gemm_b1_f8_supported(kp)) p->b1_tc = 2;
-    else if (strcmp(env, "i8pair") == 0) p->b1_tc = 3;
-    else if (strcmp(env, "f4") == 0 && tcbf::gemm_b1_f4_supported(kp)) p->b1_tc = 4;
-    else if (strcmp(env, "bmma") == 0) p->b1_tc = 5;
-    else if (strcmp(env, "f4pair") == 0 && tcbf::gemm_b1_f4_supported(kp)) p->b1_tc = 6;
-  }
+  choose_kernels(p);
   *plan = p;
   return TCBF_OK;
 }
@@ -214,34 +430,24 @@ tcbf_status tcbf_output_bytes(const tcbf_plan* plan, size_t* bytes) {
 
 const char* tcbf_plan_variant(const tcbf_plan* plan) {
   if (!plan) return "none";
-  if (plan->prec == TCBF_PREC_B1) {
-    if (!plan->b1_tc) return "b1_popc_xor_64x64";
-    if (plan->b1_tc == 5) return "b1_mma_sync_and_128x64";
-    if (plan->b1_tc == 6)
-      return plan->N % 4 ? "b1_tcgen05_mxf4pm1_2cta_256x128_stg" : "b1_tcgen05_mxf4pm1_2cta_256x128_tma";
-    if (plan->b1_tc == 2) return plan->N % 4 ? "b1_tcgen05_f8pm1_128x128_stg" : "b1_tcgen05_f8pm1_128x128_tma";
-    if (plan->b1_tc == 3) return plan->N % 4 ? "b1_tcgen05_i8_2cta_256x128_stg" : "b1_tcgen05_i8_2cta_256x128_tma";
-    if (plan->b1_tc == 4 && tcbf::gemm_b1_f4_swap_beams(plan->M) && !getenv("TCBF_NO_SWAP"))
-      return tcbf::gemm_b1_f4_swap_beams(plan->M) == 32
-                 ? (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x32_stg" : "b1_tcgen05_mxf4pm1_swap_128x32_tma")
-                 : (plan->N % 4 ? "b1_tcgen05_mxf4pm1_swap_128x64_stg" : "b1_tcgen05_mxf4pm1_swap_128x64_tma");
-    if (plan->b1_tc == 4) {
-      const char* at = getenv("TCBF_B1_ATMEM");
-      if (at && atoi(at) == 0)
-        return plan->N % 4 ? "b1_tcgen05_mxf4pm1_128x128_stg" : "b1_tcgen05_mxf4pm1_128x128_tma";
-      return plan->N % 4 ? "b1_tcgen05_mxf4pm1_atmem_128x128_stg" : "b1_tcgen05_mxf4pm1_atmem_128x128_tma";
-    }
-    return plan->N % 4 ? "b1_tcgen05_i8_128x128_stg" : "b1_tcgen05_i8_128x128_tma";
-  }
-  static const char* names[tcbf::F16_V_COUNT] = {
-      "f16_tcgen05_128x128_k32s4e8_tma", "f16_tcgen05_128x128_k64s3e4_tma", "f16_tcgen05_128x128_k64s2e8_tma",
-      "f16_tcgen05_128x128_k32s6e4_tma", "f16_tcgen05_128x64_k64s4e4_tma", "f16_tcgen05_128x128_k64s3e4_stg256",
-      "f16_tcgen05_128x128_k64s3e8_stg256", "f16_tcgen05_2cta_256x128_k64s4_tma", "f16_tcgen05_2cta_256x256_k64s3_tma",
-      "f16_tcgen05_128x128_k64s3e4_stgco", "f16_tcgen05_128x128_k64s2e8_stgco", "f16_tcgen05_128x128_k64s3e4_coop"};
-  if (plan->N % 8 != 0 && plan->N % 4 != 0) return plan->f16_variant == tcbf::F16_V_N64 ? "f16_tcgen05_128x64_masked"
-                                                                                      : "f16_tcgen05_128x128_masked";
-  return names[plan->f16_variant];
+  return gemm_kernel_name(plan);
 }
+
+const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
+  if (!plan) return "none";
+  switch (entry) {
+    case TCBF_ENTRY_BEAMFORM: return gemm_kernel_name(plan);
+    case TCBF_ENTRY_BEAMFORM_RAW:
+      if (plan->raw_mode == TCBF_RAW_FUSED) return "f16_tcgen05_fused_pack_bres_128x128";
+      if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
+      return gemm_kernel_name(plan);  // preceded by the pack kernel
+    case TCBF_ENTRY_BEAMFORM_F16I:
+      return plan->prec == TCBF_PREC_F16 ? "f16_tcgen05_interleaved_128x64" : "none";
+  }
+  return "none";
+}
+
+int tcbf_plan_raw_fused(const tcbf_plan* plan) { return plan && plan->raw_mode != TCBF_RAW_PACK ? 1 : 0; }
 
 tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* src, tcbf_src_layout layout,
                       void* dst, void* stream) {
@@ -262,11 +468,13 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
     e = tcbf::launch_pack_f16(src, (int)layout, (int)operand, plan->B, R, C,
                               operand == TCBF_WEIGHTS ? plan->kp : plan->n_packed, static_cast<uint16_t*>(dst), st);
   else
-    e = tcbf::launch_pack_b1(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, static_cast<uint32_t*>(dst), st);
+    e = tcbf::launch_pack_b1(src, (int)layout, (int)operand, plan->B, R, C, plan->kp, plan->pack_wpt,
+                             static_cast<uint32_t*>(dst), st);
   if (e != cudaSuccess) return cuda_fail(e, "pack kernel launch");
   g_launches = 1;
   return TCBF_OK;
 }
+
 
 tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed, void* out, void* stream) {
   g_launches = 0;
@@ -276,165 +484,9 @@ tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const voi
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  if (plan->prec == TCBF_PREC_F16) {
-    // Final kernel choice first, so the tensor-map boxes always match the instantiation:
-    // TMA bulk store needs N % 4 == 0 (16-B row stride), direct 256-bit stores N % 8 == 0,
-    // otherwise the masked-store epilogue (instantiated for the N64 and K64_S3 tiles only).
-    int var = plan->f16_variant;
-    const bool direct = var == tcbf::F16_V_K64_S3_DIRECT || var == tcbf::F16_V_K64_S3_DIRECT_E8;
-    const bool stgco = var == tcbf::F16_V_K64_S3_STG || var == tcbf::F16_V_K64_S3_STG_E8;
-    const bool coop = var == tcbf::F16_V_K64_S3_COOP;
-    int epi = direct ? 1 : (stgco ? 3 : (coop ? 4 : 0));
-    if (plan->N % 4 != 0) {
-      epi = 2;
-      if (var != tcbf::F16_V_N64) var = tcbf::F16_V_K64_S3;
-    } else if (direct && plan->N % 8 != 0) {
-      epi = 0;
-      var = tcbf::F16_V_K64_S3;
-    }
-    const int bn = tcbf::gemm_f16_block_n(var);
-    const int bk = tcbf::gemm_f16_block_k(var);
-    const bool tma_store = epi == 0;
-    CUtensorMap ta, tb, tc;
-    // A (weights, K-major [2B][M][K16]): box {BK, 128}, swizzle = BK * 2 bytes
-    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
-                  bk == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-    if (s != TCBF_OK) return s;
-    // B (data, MN-major [2B][K][Np]): box {64 columns, BK rows}, 128-byte swizzle; K tail is OOB -> 0
-    s = encode_3d(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_packed, plan->n_packed, plan->K, 2 * plan->B, 64, bk,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-    if (s != TCBF_OK) return s;
-    if (tma_store || epi == 4) {
-      s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32,
-                    epi == 4 ? 128 : 32, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-      if (s != TCBF_OK) return s;
-    } else {
-      memset(&tc, 0, sizeof(tc));
-    }
-    tcbf::GemmF16Args a;
-    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
-    const bool use_pair = var == tcbf::F16_V_2CTA_N128 || var == tcbf::F16_V_2CTA_N256;
-    a.tiles_m = (int)((plan->M + (use_pair ? 255 : 127)) / (use_pair ? 256 : 128));
-    a.tiles_n = (int)((plan->N + bn - 1) / bn);
-    const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
-    if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
-    a.num_tiles = (int)nt;
-    a.num_kb = (int)(plan->kp / bk);
-    a.out = static_cast<float*>(out);
-    {  // rasterisation group: keep ~48 MB of weight rows (A_r + A_i, K16 fp16) of a group in L2
-      const int64_t rows_per_tile = use_pair ? 256 : 128;
-      const int64_t bytes_per_tile_row = rows_per_tile * plan->kp * 4;
-      int64_t gm = (48ll << 20) / (bytes_per_tile_row > 0 ? bytes_per_tile_row : 1);
-      a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>(gm, a.tiles_m));
-    }
-    a.debug = 0;
-    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
-    if (use_pair)
-      e = tcbf::launch_gemm_f16_2cta(ta, tb, tc, a, bn, plan->num_sms, st);
-    else
-      e = tcbf::launch_gemm_f16(ta, tb, tc, a, var, epi, plan->num_sms, st);
-  } else {
-    tcbf::GemmB1Args a;
-    a.w = static_cast<const uint32_t*>(w_packed);
-    a.x = static_cast<const uint32_t*>(x_packed);
-    a.out = static_cast<int32_t*>(out);
-    a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
-    a.debug = 0;
-    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
-    {  // rasterisation group: 1-bit operands are small; ~16 MB of packed weight rows per group
-      const int64_t bytes_per_tile_row = 128 * plan->kp * 8;
-      const int64_t tm = (plan->M + 127) / 128;
-      a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bytes_per_tile_row, tm));
-    }
-    a.splits = 1;
-    a.kb_per_split = (int)(plan->kp / 4);
-    if (plan->b1_tc == 1) {
-      // split-K (exact int32 partials combined with TMA reduce-add)
-      const int64_t tiles = ((plan->M + 127) / 128) * ((plan->N + 127) / 128) * plan->B;
-      const int64_t nkb = plan->kp / 4;
-      // Measured: splitting does not shorten the per-SM chain of K blocks (the same total K-block
-      // count is spread over the SMs), so it is off by default and only forced for tests.
-      (void)tiles;
-      if (const char* env = getenv("TCBF_B1_SPLITS")) {
-        int64_t sp = std::min<int64_t>(std::max(1, atoi(env)), nkb);
-        if (sp > 1) {
-          a.kb_per_split = (int)((nkb + sp - 1) / sp);
-          a.splits = (int)((nkb + a.kb_per_split - 1) / a.kb_per_split);
-        }
-      }
-    }
-    if (a.splits > 1) {
-      e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
-    }
-    if (plan->b1_tc == 5) {
-      e = tcbf::launch_gemm_b1_mma(a, st);
-    } else if (plan->b1_tc) {
-      const bool tma_store = (plan->N % 4) == 0;
-      CUtensorMap tc;
-      memset(&tc, 0, sizeof(tc));
-      if (tma_store) {  // per-warp 32-row x 32-column boxes
-        s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-        if (s != TCBF_OK) return s;
-      }
-      if (plan->b1_tc == 3 || plan->b1_tc == 6) {  // CTA pair: 256-row pair tiles
-        const int64_t bpr = 256 * plan->kp * 8;
-        a.group_m = (int)std::max<int64_t>(1, std::min<int64_t>((16ll << 20) / bpr, (plan->M + 255) / 256));
-      }
-      const int swap_tm = plan->b1_tc == 4 && getenv("TCBF_NO_SWAP") == nullptr
-                              ? tcbf::gemm_b1_f4_swap_beams(plan->M) : 0;
-      if (plan->b1_tc == 6) {
-        e = tcbf::launch_gemm_b1_f4_2cta(tc, a, tma_store, plan->num_sms, st);
-      } else if (swap_tm) {  // few beams: samples on the 128-row MMA dimension, beams on N
-        CUtensorMap tw, tx;
-        const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
-        s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw,
-                      (uint32_t)swap_tm, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-        if (s != TCBF_OK) return s;
-        s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-        if (s != TCBF_OK) return s;
-        if (tma_store) {  // 32 beams x 32 samples boxes, unswizzled 128-byte rows
-          s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-          if (s != TCBF_OK) return s;
-        }
-        e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, tma_store, plan->num_sms, st);
-      } else if (plan->b1_tc == 4) {  // packed words by TMA: box {one 256-bit K block, 128 rows}
-        CUtensorMap tw, tx;
-        if (tma_store && tcbf::gemm_b1_f4_store_box_cols(plan->kp) == 16) {  // 32 x 16 boxes, 64-byte swizzle
-          s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 16, 32,
-                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-          if (s != TCBF_OK) return s;
-        }
-        const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
-        s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw, 128,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-        if (s != TCBF_OK) return s;
-        s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
-                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-        if (s != TCBF_OK) return s;
-        e = tcbf::launch_gemm_b1_f4(tw, tx, tc, a, tma_store, plan->num_sms, st);
-      } else {
-        e = plan->b1_tc == 2   ? tcbf::launch_gemm_b1_f8(tc, a, tma_store, plan->num_sms, st)
-            : plan->b1_tc == 3 ? tcbf::launch_gemm_b1_2cta(tc, a, tma_store, plan->num_sms, st)
-                               : tcbf::launch_gemm_b1_tc(tc, a, tma_store, plan->num_sms, st);
-      }
-    } else {
-      e = tcbf::launch_gemm_b1_popc(a, st);
-    }
-    if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
-    g_launches = a.splits > 1 ? 2 : 1;  // memset + kernel when split-K
-    return TCBF_OK;
-  }
-  if (e != cudaSuccess) return cuda_fail(e, "beamform kernel launch");
-  g_launches = 1;
-  return TCBF_OK;
+  return plan->prec == TCBF_PREC_F16 ? beamform_f16(plan, w_packed, x_packed, out, st)
+                                     : beamform_b1(plan, w_packed, x_packed, out, st);
 }
-
 
 tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
                               tcbf_src_layout layout, void* out, void* stream) {
@@ -446,9 +498,7 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  bool fused = plan->prec == TCBF_PREC_F16 && tcbf::gemm_f16_fused_supported(plan->kp, plan->N);
-  if (const char* env = getenv("TCBF_NO_FUSED")) fused = fused && atoi(env) == 0;
-  if (fused) {
+  if (plan->raw_mode == TCBF_RAW_FUSED) {
     CUtensorMap ta, tc;
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
@@ -463,28 +513,20 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     a.tiles_n = (int)((plan->N + 127) / 128);
     a.num_kb = (int)(plan->kp / 64);
     const int64_t nu = (int64_t)a.tiles_n * plan->B;
-    if (nu > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
+    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
     a.num_tiles = (int)(nu * a.tiles_m);
     a.out = static_cast<float*>(out);
-    if (const char* env = getenv("TCBF_DEBUG")) a.debug = atoi(env);
+    a.debug = plan->debug;
+#ifdef TCBF_DEV
     const char* trace_file = getenv("TCBF_TRACE");  // dev timeline of the fused kernel
     if (trace_file) {
       cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
       cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
     }
-    // CTA-pair variant (M=256 MMAs, data half resident per CTA, double-buffered): bit-identical
-    // but measured no faster on radio (665 vs 643 us: the tile loop is bound by the tensor rate
-    // and the HBM stores under one power budget, not by shared memory), so it is opt-in
-    // (TCBF_F16_FUSED=2)
-    const bool pair = plan->M >= 256 && nu >= 2 && getenv("TCBF_F16_FUSED") && atoi(getenv("TCBF_F16_FUSED")) == 2;
-    cudaError_t e;
-    if (pair) {
-      a.tiles_m = (int)((plan->M + 255) / 256);
-      a.num_tiles = (int)(nu * a.tiles_m);
-      e = tcbf::launch_gemm_f16_fused2(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
-    } else {
-      e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->num_sms, st);
-    }
+#endif
+    cudaError_t e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->f16_multicast != 0,
+                                                plan->num_sms, st);
+#ifdef TCBF_DEV
     if (trace_file) {
       std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
       cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
@@ -495,44 +537,14 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
         fclose(f);
       }
     }
+#endif
     if (e != cudaSuccess) return cuda_fail(e, "fused beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;
   }
-  // 1-bit fused kernel (data quantised + packed inside the GEMM): bit-exact but measured slower
-  // than pack + GEMM on radio b1 (4.4 vs 2.8 ms: its converters cannot keep enough loads in
-  // flight beside the expanded stages), so it is opt-in.
-  bool b1_fused = plan->prec == TCBF_PREC_B1 && plan->b1_tc == 1 &&
-                  tcbf::gemm_b1_fused_supported(plan->kp, plan->N) && getenv("TCBF_B1_FUSED") != nullptr;
-  if (b1_fused) {
-    CUtensorMap tc;
-    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-    if (s != TCBF_OK) return s;
-    tcbf::GemmB1Args a;
-    memset(&a, 0, sizeof(a));
-    a.w = static_cast<const uint32_t*>(w_packed);
-    a.out = static_cast<int32_t*>(out);
-    a.M = (int)plan->M; a.N = (int)plan->N; a.K = (int)plan->K; a.Kw = (int)plan->kp; a.B = (int)plan->B;
-    a.splits = 1;
-    cudaError_t e = tcbf::launch_gemm_b1_fused(tc, a, x_src, (int)layout, plan->num_sms, st);
-    if (e != cudaSuccess) return cuda_fail(e, "fused 1-bit beamform kernel launch");
-    g_launches = 1;
-    return TCBF_OK;
-  }
-  // Small-M plans (one 128-row weight tile): every data element enters one tile, so the
-  // streaming kernel converts the fp32 data on the fly (no separate pack pass).
-  // Needs enough (batch, column) tiles to occupy the GPU (measured: 32 tiles lose to pack + GEMM).
-  // Needs enough work units (column tiles x K splits) to occupy the GPU; below a quarter of the
-  // SMs the pack + GEMM pair is kept.
-  const int64_t conv_tiles = ((plan->N + 127) / 128) * plan->B;
-  const int conv_kb = (int)((plan->K + tcbf::gemm_f16_conv_block_k() - 1) / tcbf::gemm_f16_conv_block_k());
-  const int64_t conv_units =
-      conv_tiles * (conv_tiles < INT32_MAX ? tcbf::gemm_f16_conv_splits((int)conv_tiles, conv_kb, plan->num_sms) : 1);
-  bool stream_conv = plan->prec == TCBF_PREC_F16 && plan->M <= 128 && plan->N % 4 == 0 && aligned(x_src, 16) &&
-                     (conv_units >= plan->num_sms / 4 || getenv("TCBF_FORCE_STREAM_CONV"));
-  if (const char* env = getenv("TCBF_NO_FUSED")) stream_conv = stream_conv && atoi(env) == 0;
-  if (stream_conv) {
+  if (plan->raw_mode == TCBF_RAW_STREAM && aligned(x_src, 16)) {
+    // Small-M plans (one 128-row weight tile): every data element enters one tile, so the
+    // streaming kernel converts the fp32 data on the fly (no separate pack pass).
     const int bk = tcbf::gemm_f16_conv_block_k();
     CUtensorMap ta, tx, tc;
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
@@ -560,11 +572,10 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     if (nt * 16 > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
     a.num_tiles = (int)nt;
     a.num_kb = (int)((plan->K + bk - 1) / bk);
-    a.splits = tcbf::gemm_f16_conv_splits(a.num_tiles, a.num_kb, plan->num_sms);
-    if (const char* env = getenv("TCBF_CONV_SPLITS")) a.splits = std::max(1, std::min(atoi(env), a.num_kb));
+    conv_units(plan, &a.splits);
     a.kb_per_split = (a.num_kb + a.splits - 1) / a.splits;
-    a.splits = (a.num_kb + a.kb_per_split - 1) / a.kb_per_split;
     a.out = static_cast<float*>(out);
+    a.debug = plan->debug;
     int launches = 1;
     if (a.splits > 1) {  // partial sums are reduce-added into a zeroed output
       cudaError_t e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
@@ -576,19 +587,23 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     g_launches = launches;
     return TCBF_OK;
   }
-  // Keep the stream-ordered pool's memory cached between calls (the default release threshold
-  // returns it to the driver at every synchronisation, making each call pay a fresh allocation).
+  // Pack into stream-ordered scratch, then beamform.  Keep the pool's memory cached between calls
+  // (the default release threshold returns it to the driver at every synchronisation, making each
+  // call pay a fresh allocation).
   retain_pool_memory();
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, plan->x_bytes, st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (data scratch)");
+  if (e != cudaSuccess) return fail(TCBF_ERR_ALLOC, "cudaMallocAsync (data scratch): %s", cudaGetErrorString(e));
   s = tcbf_pack(plan, TCBF_DATA, x_src, layout, scratch, stream);
-  if (s == TCBF_OK) s = tcbf_beamform(plan, w_packed, scratch, out, stream);
+  int launches = s == TCBF_OK ? 1 : 0;
+  if (s == TCBF_OK) {
+    s = tcbf_beamform(plan, w_packed, scratch, out, stream);
+    launches += g_launches;
+  }
   cudaFreeAsync(scratch, st);
-  g_launches = s == TCBF_OK ? 2 : 0;
+  g_launches = s == TCBF_OK ? launches : 0;
   return s;
 }
-
 tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, const void* x_f16, void* out,
                                void* stream) {
   g_launches = 0;

@@ -4,6 +4,7 @@ import ctypes
 import os
 import re
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -88,3 +89,21 @@ def test_null_plan_arguments(tcbf):
     assert L.tcbf_pack(None, 0, None, 0, None, None) == 1
     assert L.tcbf_beamform(None, None, None, None, None) == 1
     assert L.tcbf_beamform_host(None, None, None, 0, None) == 1
+
+
+def test_product_library_has_no_dev_switches(tcbf):
+    """The ablation / trace switches of the DESIGN.md §4 studies exist only in TCBF_DEV builds:
+    the product library cannot be put into a wrong-result mode by the environment."""
+    data = open(tcbf.library_path, "rb").read()
+    for s in (b"TCBF_DEBUG", b"TCBF_TRACE"):
+        assert s not in data, s
+
+
+def test_binding_validates_tensors_before_the_abi():
+    """Raw pointers cross the ABI only for contiguous CUDA tensors of the right dtype and size."""
+    import torch
+    from paper_2505_03269_b200 import _need
+    with pytest.raises(ValueError, match="CUDA"):
+        _need(torch.zeros(4), "x", ("f32",), 16)
+    with pytest.raises(TypeError):
+        _need(np.zeros(4, np.float32), "x", ("f32",), 16)
