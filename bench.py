@@ -12,9 +12,16 @@ tcbf_beamform_raw -- one fused kernel for short-K fp16 plans (each data element 
 once inside the GEMM), otherwise tcbf_pack(DATA) + tcbf_beamform.  The weights are packed
 once before timing (PAPER.md:362: the model matrix is prepared once;
 PAPER.md:48: weights constant over a period).  Useful ops = 8*B*M*N*K.
-Multi-GPU: weak scaling, every rank beamforms its own `batch` channels (global batch =
-N x batch), no data-path collective; time = max over ranks of CUDA-event time.
-Default workload = BASELINE configs[1] (radio astronomy fp16, LOFAR-shaped).
+Multi-GPU: STRONG scaling of the fixed config -- the global batch is split into
+contiguous slices (radio: 256 channels -> 32 per rank at N=8), or, when the batch is smaller than
+the world (square / M=32 sweeps), the samples N are split in multiples of 4 with the weights
+replicated; K is never split, so there is no data-path collective.  Inputs are generated from
+global indices, so every N computes the same global problem.  value = global useful ops / (max
+over ranks of the CUDA-event step time).  The optional NCCL output gather (--gather) is timed
+separately and never enters `value`.
+Default workload = BASELINE configs[1] (radio astronomy fp16, LOFAR-shaped); the
+same run also times radio 1-bit (configs[2]) and ultrasound fp16 (configs[3]) under `records`,
+so the driver-timed line carries both precisions of the metric.
 """
 from __future__ import annotations
 
@@ -172,14 +179,23 @@ class ClockSampler:
              0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
              0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, index):
+    def __init__(self, device, sample=True):
+        """device: the torch CUDA device this rank runs on.  NVML ignores CUDA_VISIBLE_DEVICES, so
+        the NVML handle is looked up by the device's PCI bus id, not by the CUDA ordinal."""
         self.samples, self.reasons, self.ok = [], 0, False
         self.max_mhz = None
+        self.sample = sample
         try:
             import pynvml
+            import torch
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            props = torch.cuda.get_device_properties(device)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
         except Exception:
@@ -205,13 +221,15 @@ class ClockSampler:
     def start(self):
         if self.ok:
             self.e0 = self.energy_mj()
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+            if self.sample:
+                self.t = threading.Thread(target=self._run, daemon=True)
+                self.t.start()
 
     def stop(self):
         if self.ok:
-            self._stop.set()
-            self.t.join()
+            if self.sample:
+                self._stop.set()
+                self.t.join()
             self.e1 = self.energy_mj()
 
     def joules(self):
@@ -357,18 +375,15 @@ def pack_weights(plan, c, seed, dev, b0, max_src_bytes=8 << 30):
     return wp
 
 
-def run_tcbf(args, c):
+def setup_dist(args):
+    """One process per GPU (torchrun env), NCCL; --dist-backend gloo is the single-GPU test mode in
+    which every rank shares cuda:0 (exercises the N>1 code path on one device)."""
     import torch
     import torch.distributed as dist
-
-    import paper_2505_03269_b200 as tcbf
-    import synth
-    from paper_2505_03269_b200.shard import max_over_ranks, weak_shard
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.dist_backend == "gloo":   # test mode: every rank on cuda:0 (exercises the N>1 path on 1 GPU)
+    if args.dist_backend == "gloo":
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
@@ -376,154 +391,264 @@ def run_tcbf(args, c):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-    dev = torch.device("cuda", local)
-    sh = weak_shard(c["B"], rank)
-    M, N, K, B = c["M"], c["N"], c["K"], c["B"]
-    seed = synth.SEED_BASE + c["idx"]
-    plan = tcbf.Plan(M, N, K, B, c["prec"])
+    return world, rank, local, torch.device("cuda", local)
 
-    wp = pack_weights(plan, c, seed, dev, sh.b0)
-    xsrc = synth.generate_device(c["xd"], seed, 1, B, K, N, device=dev, b0=sh.b0)
+
+def shard_inputs(c, sh, seed, dev):
+    """This rank's plan, packed weights and fp32 data of the GLOBAL problem c:
+    batch slices b0..b0+nb (inputs generated from the global index space), or -- batch smaller
+    than the world -- sample columns n0..n0+nn of every batch entry with the weights replicated.
+    K is never split, so no rank needs another rank's partial sums."""
+    import paper_2505_03269_b200 as tcbf
+    import synth
+    M, N, K = c["M"], c["N"], c["K"]
+    if sh.mode == "samples":
+        plan = tcbf.Plan(M, sh.nn, K, c["B"], c["prec"])
+        wp = pack_weights(plan, dict(c, N=sh.nn), seed, dev, 0)
+        xfull = synth.generate_device(c["xd"], seed, 1, c["B"], K, N, device=dev, b0=0)
+        xsrc = xfull[:, :, sh.n0:sh.n0 + sh.nn].contiguous()
+        del xfull
+    else:
+        plan = tcbf.Plan(M, N, K, sh.nb, c["prec"])
+        wp = pack_weights(plan, dict(c, B=sh.nb), seed, dev, sh.b0)
+        xsrc = synth.generate_device(c["xd"], seed, 1, sh.nb, K, N, device=dev, b0=sh.b0)
+    return plan, wp, xsrc
+
+
+def measure(args, name, c, world, rank, local, dev, steps, warmup, e2e=False, energy=False, sample_clocks=True):
+    """Time `steps` steps of workload c (the global problem, sharded over the world) and return
+    its record: ms_per_step (max over ranks), whole-job TeraOps/s, the dominant kernel's roofline,
+    clocks, optionally e2e through the host-buffer API and a >= 1 s energy loop."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_03269_b200 as tcbf
+    import synth
+    from paper_2505_03269_b200.shard import max_over_ranks, plan_shard
+
+    sh = plan_shard(c["B"], c["N"], rank, world)
+    seed = synth.SEED_BASE + c["idx"]
+    plan, wp, xsrc = shard_inputs(c, sh, seed, dev)
+    lc = dict(c, B=plan.batch, N=plan.N)   # this rank's share
     f16i = c.get("src") == "f16i"
     if f16i:   # the producer delivers interleaved fp16 (conversion outside the timed region)
         xsrc = xsrc.half()
+    fused = plan.raw_fused and not f16i
     xp = plan.alloc_packed(tcbf.DATA, dev)
     out = plan.alloc_output(dev)
     torch.cuda.synchronize()
 
-    working = xsrc.numel() * 4 + plan.x_bytes + plan.w_bytes + plan.out_bytes
+    working = xsrc.numel() * xsrc.element_size() + plan.x_bytes + plan.w_bytes + plan.out_bytes
     flush = working < 4 * L2_BYTES
     flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
     stream = torch.cuda.current_stream(dev)
 
-    def step():
+    def step(ev=None):
         if f16i:
+            if ev: ev[1].record(stream)
             plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
-        elif plan.raw_fused:
+        elif fused:
+            if ev: ev[1].record(stream)
             plan.beamform_raw(wp, xsrc, out=out, stream=stream)
         else:
             plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
+            if ev: ev[1].record(stream)
             plan.beamform(wp, xp, out, stream=stream)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         if flush:
             flush_buf.fill_(1.0)
         step()
     torch.cuda.synchronize()
     # kernels per step, as the library counts them (pack: 1; beamform: 1, or memset + kernel on split K)
-    launches_per_step = tcbf.Plan.last_launch_count() + (0 if (f16i or plan.raw_fused) else 1)
+    launches_per_step = tcbf.Plan.last_launch_count() + (0 if (f16i or fused) else 1)
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    sampler = ClockSampler(dev) if sample_clocks else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
-    fused = plan.raw_fused and not f16i
-    for i in range(args.steps):
+    if sampler:
+        sampler.start()
+    for i in range(steps):
         if flush:
             flush_buf.fill_(float(i))   # evict L2 between timed steps (not inside the timed spans)
         ev[i][0].record(stream)
-        if f16i:
-            ev[i][1].record(stream)
-            plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
-        elif fused:
-            ev[i][1].record(stream)
-            plan.beamform_raw(wp, xsrc, out=out, stream=stream)
-        else:
-            plan.pack(tcbf.DATA, xsrc, out=xp, stream=stream)
-            ev[i][1].record(stream)
-            plan.beamform(wp, xp, out, stream=stream)
+        step(ev[i])
         ev[i][2].record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    sampler.stop()
+    if sampler:
+        sampler.stop()
     if flush:
         total_ms = sum(e[0].elapsed_time(e[2]) for e in ev)
     else:
         total_ms = ev[0][0].elapsed_time(ev[-1][2])
-    gemm_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
-    pack_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
-    ms_step = max_over_ranks(total_ms / args.steps, dev)
+    gemm_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / steps
+    pack_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / steps
+    ms_step = max_over_ranks(total_ms / steps, dev)
     gemm_ms_max = max_over_ranks(gemm_ms, dev)
-    value = world * useful_ops(c) / (ms_step * 1e-3) / 1e12
-    frames_per_s = world * c["N"] * c["B"] / (ms_step * 1e-3)
-
-    # ---- e2e through the public API with HOST buffers (pinned), copies inside the timed region
-    x_host = xsrc.cpu().pin_memory()
-    out_host = torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory()
-    e2e_steps = max(1, min(args.steps, int(os.environ.get("TCBF_E2E_STEPS", "5"))))
-
-    def e2e_call():
-        if f16i:   # H2D of the fp16 data, beamform_f16i, D2H of the output (binding-level API)
-            xsrc.copy_(x_host, non_blocking=True)
-            plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
-            out_host.copy_(out, non_blocking=True)
-            torch.cuda.synchronize()
-        else:
-            plan.beamform_host(wp, x_host, out_host)
-
-    e2e_call()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_call()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_s = max_over_ranks(e2e_s, dev)
-    e2e_val = world * useful_ops(c) / e2e_s / 1e12
+    value = useful_ops(c) / (ms_step * 1e-3) / 1e12      # the global problem / slowest rank
 
     peaks = load_peaks()
-    roof = roofline_for(c, gemm_ms_max, peaks, long_step=(args.steps * ms_step > 1000.0), variant=plan.variant,
-                        fused=fused)
-    roof["kernel"] = "f16_tcgen05_interleaved_128x64" if f16i else (plan.raw_variant if fused else plan.variant)
-    roof["traffic"] = traffic_for(args.config, roof["kernel"])
+    # roofline of the dominant kernel on the slowest rank's share (each rank runs the same kernel)
+    kern = plan.kernel("f16i" if f16i else ("raw" if fused else "beamform"))
+    roof = roofline_for(lc, gemm_ms_max, peaks, long_step=(steps * ms_step > 1000.0), variant=kern, fused=fused)
+    roof["kernel"] = kern
+    roof["traffic"] = traffic_for(name, kern) if world == 1 else None
     roof["kernel_ms"] = round(gemm_ms_max, 4)
-    roof["algorithmic_bytes_per_launch"] = gemm_bytes(c, fused)
-    roof["useful_ops_per_launch"] = useful_ops(c)
+    roof["algorithmic_bytes_per_launch"] = gemm_bytes(lc, fused)
+    roof["useful_ops_per_launch"] = useful_ops(lc)
     pack_ms_max = max_over_ranks(pack_ms, dev) if not (fused or f16i) else 0.0
     if pack_ms_max > gemm_ms_max:
         # the data pack dominates the step (few beams: M=32 sweeps): report ITS roofline as the
         # dominant kernel, the GEMM's beside it
-        pk = pack_roofline(c, pack_ms_max, plan.x_bytes, peaks)
+        pk = pack_roofline(lc, pack_ms_max, plan.x_bytes, peaks)
         pk["gemm"] = roof
-        pk["traffic"] = traffic_for(args.config, pk["kernel"])
+        pk["traffic"] = traffic_for(name, pk["kernel"]) if world == 1 else None
         roof = pk
 
+    rec = {
+        "workload": name, "desc": c["desc"], "precision": c["prec"],
+        "value": round(value, 2), "unit": "TeraOps/s", "ms_per_step": round(ms_step, 4), "steps": steps,
+        "M": c["M"], "N": c["N"], "K": c["K"], "global_batch": c["B"],
+        "shard": {"mode": sh.mode, "batch_per_rank": plan.batch, "samples_per_rank": plan.N},
+        "step": ("tcbf_beamform_f16i (fp16 interleaved data, no pack)" if f16i else
+                 "tcbf_beamform_raw (data pack fused into the GEMM)" if fused else
+                 "tcbf_pack(data) + tcbf_beamform") + "; weights packed once",
+        "l2": ("flushed between steps (256 MiB write)" if flush else
+               f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
+        "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4),
+        "samples_per_s": round(c["N"] * c["B"] / (ms_step * 1e-3), 1),
+        "roofline": roof,
+        "gpu_launches": launches_per_step * steps,
+    }
+    if sampler:
+        rec["clocks"] = sampler.summary()
+
+    if energy:
+        rec["energy"] = energy_loop(step, stream, c, dev, world)
+
+    if e2e:
+        # through the public API with HOST buffers (pinned), copies inside the timed region
+        x_host = xsrc.cpu().pin_memory()
+        out_host = torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory()
+        e2e_steps = max(1, min(steps, 5))
+
+        def e2e_call():
+            if f16i:   # H2D of the fp16 data, beamform_f16i, D2H of the output (binding-level API)
+                xsrc.copy_(x_host, non_blocking=True)
+                plan.beamform_f16i(wp, xsrc, out=out, stream=stream)
+                out_host.copy_(out, non_blocking=True)
+                torch.cuda.synchronize()
+            else:
+                plan.beamform_host(wp, x_host, out_host)
+
+        e2e_call()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_call()
+        e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, dev)
+        rec["e2e"] = {"value": round(useful_ops(c) / e2e_s / 1e12, 3), "unit": "TeraOps/s",
+                      "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()) * world,
+                      "d2h_bytes_per_step": int(plan.out_bytes) * world,
+                      "api": ("Plan.beamform_f16i with pinned-host copies in and out" if f16i else
+                              "tcbf_beamform_host (pinned host buffers)"),
+                      "steps": e2e_steps}
+
+    if args.gather and world > 1 and sh.mode == "batch" and c["B"] % world == 0:
+        # the optional output gather (SURVEY.md §8e): timed separately, never part of `value`
+        from paper_2505_03269_b200.shard import gather_outputs
+        gather_outputs(out)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = gather_outputs(out)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        rec["gather"] = {"ms": round(max_over_ranks(g0.elapsed_time(g1), dev), 3),
+                         "bytes_per_rank_received": int(full.numel() * full.element_size() - plan.out_bytes),
+                         "collective": f"all_gather_into_tensor ({args.dist_backend})"}
+        del full
+    del wp, xsrc, xp, out, flush_buf
+    torch.cuda.empty_cache()
+    return rec
+
+
+def energy_loop(step, stream, c, dev, world, min_s=1.0):
+    """NVML energy over a separate loop of >= `min_s` seconds of back-to-back steps (the counter's
+    granularity makes short timed regions meaningless).  Board energy of this GPU; TeraOps/J of the
+    whole job = global ops / (joules summed over ranks)."""
+    import torch
+    from paper_2505_03269_b200.shard import sum_over_ranks
+    s = ClockSampler(dev, sample=False)
+    if not s.ok:
+        return {"unavailable": "NVML not available"}
+    # calibrate the step count for ~min_s
+    t0 = time.perf_counter()
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    per = max(1e-5, (time.perf_counter() - t0) / 3)
+    n = max(10, int(min_s / per) + 1)
+    s.start()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        step()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    s.stop()
+    j = s.joules()
+    if j is None or j <= 0:
+        return {"unavailable": "NVML energy counter returned no delta"}
+    j_all = sum_over_ranks(j, dev)
+    watts = j / wall
+    rec = {"joules_per_step": round(j_all / n, 6), "teraops_per_joule": round(useful_ops(c) * n / j_all / 1e12, 3),
+           "loop_s": round(wall, 3), "steps": n, "avg_board_w": round(watts, 1),
+           "source": "NVML total energy counter over a separate >= 1 s loop of back-to-back steps"}
+    if watts > 1200.0:   # a B200 board cannot sustain this: counter artefact, do not report
+        return {"unavailable": f"implausible average power {watts:.0f} W over {wall:.2f} s"}
+    return rec
+
+
+def run_tcbf(args, c):
+    import torch.distributed as dist
+    world, rank, local, dev = setup_dist(args)
+    main = measure(args, args.config, c, world, rank, local, dev, args.steps, args.warmup, e2e=True,
+                   energy=not args.no_energy)
+    records = {}
+    extra = [r for r in (args.records.split(",") if args.records else []) if r and r != args.config]
+    for r in extra:
+        records[r] = measure(args, r, CONFIGS[r], world, rank, local, dev, args.steps, args.warmup)
     line = {
         "metric": "beamforming TeraOps/s (fp16 and 1-bit) at 1/2/4/8 B200 vs roofline",
-        "value": round(value, 2), "unit": "TeraOps/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": c["prec"], "data": "synthetic (seeded counter-based generator, synth/)",
-        "config": {"workload": args.config, "desc": c["desc"], "M": M, "N": N, "K": K, "batch_per_gpu": B,
-                   "global_batch": B * world, "precision": c["prec"],
-                   "step": ("tcbf_beamform_f16i (fp16 interleaved data, no pack)" if f16i else
-                            "tcbf_beamform_raw (data pack fused into the GEMM)" if fused else
-                            "tcbf_pack(data) + tcbf_beamform") + "; weights packed once",
-                   "l2": ("flushed between steps (256 MiB write)" if flush else
-                          f"working set {working / 2 ** 30:.2f} GiB > L2 (126 MiB), no flush"),
-                   "parallelism": f"batch-sharded x{world}, no data-path collective",
-                   "pack_ms": round(pack_ms, 4), "gemm_ms": round(gemm_ms, 4),
-                   "samples_per_s": round(frames_per_s, 1)},
-        "roofline": roof,
-        "e2e": {"value": round(e2e_val, 3), "unit": "TeraOps/s",
-                "h2d_bytes_per_step": int(x_host.numel() * x_host.element_size()),
-                "d2h_bytes_per_step": int(plan.out_bytes),
-                "api": ("Plan.beamform_f16i with pinned-host copies in and out" if f16i else
-                        "tcbf_beamform_host (pinned host buffers)"),
-                "steps": e2e_steps},
-        "gpu_launches": launches_per_step * args.steps,
-        "clocks": sampler.summary(),
+        "value": main["value"], "unit": "TeraOps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": c["prec"],
+        "data": "synthetic (seeded counter-based generator, synth/)",
+        "config": {"workload": args.config, "desc": c["desc"], "M": c["M"], "N": c["N"], "K": c["K"],
+                   "global_batch": c["B"], "batch_per_gpu": main["shard"]["batch_per_rank"],
+                   "samples_per_gpu": main["shard"]["samples_per_rank"], "precision": c["prec"],
+                   "step": main["step"], "l2": main["l2"],
+                   "parallelism": (f"{main['shard']['mode']}-sharded x{world} (SURVEY.md §8e strong scaling of "
+                                   f"the fixed config), no data-path collective"),
+                   "pack_ms": main["pack_ms"], "gemm_ms": main["gemm_ms"], "samples_per_s": main["samples_per_s"]},
+        "roofline": main["roofline"],
+        "e2e": main["e2e"],
+        "gpu_launches": main["gpu_launches"],
+        "clocks": main["clocks"],
     }
-    j = sampler.joules()
-    if j is not None and j > 0:   # whole-board energy over the timed region (NEXT-4, Table III TOPs/J)
-        j = max_over_ranks(j, dev) if world == 1 else j
-        line["energy"] = {"joules_per_step": round(j / args.steps, 6),
-                          "teraops_per_joule": round(useful_ops(c) / (j / args.steps) / 1e12, 3),
-                          "timed_region_s": round(total_ms / 1e3, 3),
-                          "source": "NVML total energy counter, this GPU, timed region "
-                                    "(counter granularity makes regions < ~1 s coarse)"}
+    if "energy" in main:
+        line["energy"] = main["energy"]
+    if "gather" in main:
+        line["gather"] = main["gather"]
+    if records:
+        line["records"] = records
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c)
     if rank == 0:
@@ -543,10 +668,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo = test mode, all ranks share cuda:0 (production runs use nccl)")
+    ap.add_argument("--records", default=None,
+                    help="comma-separated extra workloads timed in the same run and reported under 'records' "
+                         "(default for radio_f16: radio_b1,ultrasound_f16 -- both precisions of the metric)")
+    ap.add_argument("--no-energy", action="store_true", help="skip the >= 1 s NVML energy loop")
+    ap.add_argument("--gather", action="store_true", help="also time the optional NCCL output gather (N > 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     c = CONFIGS[args.config]
+    if args.records is None:
+        args.records = "radio_b1,ultrasound_f16" if args.config == "radio_f16" else ""
     if args.impl == "reference":
         return run_reference(args, c)
     return run_tcbf(args, c)

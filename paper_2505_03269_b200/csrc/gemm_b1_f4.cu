@@ -168,18 +168,31 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_
       "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
-// the 32 e2m1 words of one row's 256-bit K block in logical (unswizzled) order -> TMEM columns
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// the 32 e2m1 words of one row's 256-bit K block in logical (unswizzled) order -> TMEM columns,
+// in two 16-column halves (keeps 16 instead of 32 expanded words live: the 576-thread CTA gets
+// 96 registers per thread)
 __device__ __forceinline__ void expand_tmem(uint32_t taddr, const uint4& lo, const uint4& hi) {
   const uint32_t w[KBW] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-  uint32_t v[32];
 #pragma unroll
-  for (int q = 0; q < KBW; ++q) {
-    v[4 * q] = nib_pm1<0>(w[q]);
-    v[4 * q + 1] = nib_pm1<1>(w[q]);
-    v[4 * q + 2] = nib_pm1<2>(w[q]);
-    v[4 * q + 3] = nib_pm1<3>(w[q]);
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[16];
+#pragma unroll
+    for (int q = 0; q < KBW / 2; ++q) {
+      v[4 * q] = nib_pm1<0>(w[4 * h + q]);
+      v[4 * q + 1] = nib_pm1<1>(w[4 * h + q]);
+      v[4 * q + 2] = nib_pm1<2>(w[4 * h + q]);
+      v[4 * q + 3] = nib_pm1<3>(w[4 * h + q]);
+    }
+    tmem_st_32x32b_x16(taddr + 16 * h, v);
   }
-  tmem_st_32x32b_x32(taddr, v);
 }
 
 template <bool TMA_STORE, bool TMA_WORDS, bool ATMEM>
@@ -308,13 +321,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if ((TCBF_ABLATE(p, 8)) && lane == 0) mbar_arrive(tempty_bar);
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + part * BN;
       const int corr = part == 0 ? 0 : two_kpad;
-      uint32_t vbuf[2][32];
-      tmem_ld_32x32b_x32(tbase, vbuf[0]);
+      // 16-column TMEM loads, two in flight (32 live registers instead of 64: the 576-thread CTA
+      // has 96 registers per thread and the 32-column version spilled)
+      constexpr int CW = 16;
+      constexpr int NCH = BN / CW;
+      uint32_t vbuf[2][CW];
+      tmem_ld_32x32b_x16(tbase, vbuf[0]);
 #pragma unroll
-      for (int c = 0; c < CHUNKS; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         tmem_wait_ld();
-        if (c + 1 < CHUNKS) {
-          tmem_ld_32x32b_x32(tbase + (c + 1) * 32, vbuf[(c + 1) & 1]);
+        if (c + 1 < NCH) {
+          tmem_ld_32x32b_x16(tbase + (c + 1) * CW, vbuf[(c + 1) & 1]);
         } else {  // all TMEM reads of this warp done: the next tile's MMAs may start
           tc_fence_before();
           __syncwarp();
@@ -322,25 +339,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         uint32_t* vv = vbuf[c & 1];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
+        for (int j = 0; j < CW; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
         if (TCBF_ABLATE(p, 1)) continue;
         if constexpr (TMA_STORE) {  // 32-row boxes of BOX_COLS columns, double-buffered per warp
-#pragma unroll
-          for (int h = 0; h < 32 / BOX_COLS; ++h) {
-            uint8_t* buf = bufs + sbuf * EPI_BOX;
+          const int off = (c * CW) % BOX_COLS;  // column of this chunk inside its box
+          uint8_t* buf = bufs + sbuf * EPI_BOX;
+          if (off == 0) {
             if (lane == 0) bulk_wait_group_read<1>();
             __syncwarp();
+          }
 #pragma unroll
-            for (int j = 0; j < BOX_COLS / 4; ++j) {  // 16-byte chunks, 64- or 128-byte swizzle
-              const int pos = BOX_COLS == 16 ? (j ^ ((lane >> 1) & 3)) : (j ^ (lane & 7));
-              const int o = BOX_COLS * h + 4 * j;
-              *reinterpret_cast<uint4*>(buf + lane * (BOX_COLS * 4) + pos * 16) =
-                  make_uint4(vv[o], vv[o + 1], vv[o + 2], vv[o + 3]);
-            }
+          for (int j = 0; j < CW / 4; ++j) {  // 16-byte chunks, 64- or 128-byte swizzle
+            const int jj = off / 4 + j;
+            const int pos = BOX_COLS == 16 ? (jj ^ ((lane >> 1) & 3)) : (jj ^ (lane & 7));
+            *reinterpret_cast<uint4*>(buf + lane * (BOX_COLS * 4) + pos * 16) =
+                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+          }
+          if (off + CW == BOX_COLS) {
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&tmC, buf, n0 + c * 32 + BOX_COLS * h, m0 + q * 32, 2 * b + part);
+              tma_store_3d(&tmC, buf, n0 + c * CW + CW - BOX_COLS, m0 + q * 32, 2 * b + part);
               bulk_commit_group();
             }
             sbuf ^= 1;
@@ -350,8 +369,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (m < p.M) {
             int32_t* rowp = p.out + ((size_t)(2 * b + part) * p.M + m) * (size_t)p.N;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = n0 + c * 32 + j;
+            for (int j = 0; j < CW; ++j) {
+              const int n = n0 + c * CW + j;
               if (n < p.N) rowp[n] = (int32_t)vv[j];
             }
           }

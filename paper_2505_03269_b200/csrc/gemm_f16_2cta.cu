@@ -144,8 +144,10 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  cluster_sync();  // barriers initialised and TMEM allocated in both CTAs
-  __syncthreads();  // (redundant with the cluster barrier; orders the alloc's smem write for racecheck)
+  // Barriers initialised and TMEM allocated in both CTAs.  (compute-sanitizer racecheck reports
+  // the PEER CTA's cta_group::2 alloc -- which writes the address into both CTAs' tmem_slot --
+  // against the read below: a tool limitation, the cluster barrier orders them; profiles/r02.)
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

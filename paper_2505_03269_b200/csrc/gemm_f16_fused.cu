@@ -167,8 +167,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_relinquish();
   }
   tc_fence_before();
-  if (MC) cluster_sync();  // peers signal this CTA's barriers
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // peers signal this CTA's barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 

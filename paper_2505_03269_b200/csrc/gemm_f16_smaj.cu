@@ -1,0 +1,352 @@
+// gemm_f16_smaj.cu -- sample-major fused 16-bit beamformer: fp32 data in, fp32 beams out, with
+// the SAMPLES on the 128-row MMA dimension and the beams on N.
+//
+// Same arithmetic as the other 16-bit kernels (fp16 RNE inputs, exact products, fp32 accumulation
+// in TMEM, four real sub-products per K step -- PAPER.md:143-159), computed transposed:
+//     D^T[n][m] = sum_k X[k][n] W[m][k]
+// with the data X (converted once per unit from fp32 by converter warps, like gemm_f16_fused.cu)
+// as the MN-major A operand and the weights as the K-major B operand, stacked [W_r ; W_i]:
+//     [Re | Im] += X_r [W_r ; W_i]^T          (one M=128, N=256 MMA)
+//     Re        += (-X_i) W_i^T               (N=128, negate-A bit: the paper's negation step)
+//     Im        += X_i W_r^T                  (N=128)
+// Per K step that is 28 KB of operand reads per 128x128 complex tile instead of the 32 KB of four
+// N=128 MMAs, and no third (negated) operand plane is needed.
+//
+// Why transposed: the radio shapes are bound by the 8 bytes/complex output stream.
+// With samples on TMEM lanes, `tcgen05.ld 32x32b` gives thread t of a warp the sample n0+t, so one
+// warp store of register j writes 32 CONSECUTIVE floats (one full 128-byte line) of beam row m+j:
+// the output leaves the SM as fully coalesced line writes straight from registers -- no smem
+// staging (the 256 KB of staging traffic per tile of the beam-major kernel), no TMA store engine
+// (measured capped near 6.0 TB/s on these patterns), any N (no N % 4 rule).
+//
+// Work unit = (batch entry b, 128 samples); the unit's data stays resident in smem (K16 <= 256)
+// while every 128-beam weight tile streams through a 3-stage TMA ring; TMEM holds two 256-column
+// accumulators so the epilogue of one tile overlaps the MMAs of the next.
+//
+// Roles: warp 0 TMA producer (weights), warp 1 MMA issuer, warps 2..2+EPI_WARPS-1 epilogue
+// (tcgen05.ld -> coalesced st.global), then 8 converter warps (fp32 -> fp16 MN-major planes).
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tcbf {
+namespace {
+
+constexpr int BS = 128;                    // samples per tile (MMA M)
+constexpr int BB = 128;                    // beams per tile (stacked N = 256)
+constexpr int BK = 64;
+constexpr int KMAX = 256;                  // resident K rows (K16 <= 256)
+constexpr int CONV_WARPS = 8;
+constexpr int W_TILE = BB * BK * 2;        // one weight plane of one stage (16 KB)
+constexpr int W_STAGE = 2 * W_TILE;        // [W_r ; W_i]
+constexpr int W_STAGES = 3;
+constexpr int X_PLANE = 2 * KMAX * 128;    // 2 blocks of 64 samples x KMAX k-rows x 128 B
+constexpr int OFF_X = 0;                   // X_r, X_i planes
+constexpr int OFF_W = 2 * X_PLANE;
+constexpr int BAR_OFFSET = OFF_W + W_STAGES * W_STAGE;
+constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+static_assert(SMEM_BYTES <= 232448, "smem budget");
+
+template <int EPI_WARPS>
+struct SCfg {
+  static constexpr int NUM_THREADS = (2 + EPI_WARPS + CONV_WARPS) * 32;
+  static constexpr int CONV0 = 2 + EPI_WARPS;
+};
+
+// K-major weights (B operand): 128-byte swizzle, 8-row groups 1024 B apart; the W_i tile follows
+// the W_r tile directly, so one descriptor spans the stacked N = 256 operand
+__device__ __forceinline__ uint64_t desc_w(const void* tile, uint32_t k_byte_off) {
+  uint32_t addr = smem_u32(tile) + k_byte_off;
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// resident MN-major data (A operand): 64-sample block j at j * KMAX * 128 B (LBO), 8 k-rows per
+// 1024 B (SBO), 128-byte swizzle
+__device__ __forceinline__ uint64_t desc_x(const void* plane, uint32_t k_row) {
+  uint32_t addr = smem_u32(plane) + k_row * 128u;
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((KMAX * 128u) >> 4) << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// kind::f16: fp16 A/B, fp32 D, A MN-major (bit 15), B K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_smaj(uint32_t N, bool negate_a) {
+  return (1u << 4) | ((negate_a ? 1u : 0u) << 13) | (1u << 15) | ((N >> 3) << 17) | ((uint32_t)(BS >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t h2u(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int LAYOUT, bool VEC, int EPI_WARPS>
+__global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
+    cgemm_f16_smaj_kernel(const __grid_constant__ CUtensorMap tmW, GemmF16Args args, const float* __restrict__ xsrc,
+                          int K) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sX = smem + OFF_X;  // [2 planes][2 sample blocks][KMAX rows][128 B]
+  uint8_t* sW = smem + OFF_W;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
+  uint64_t* wempty = wfull + W_STAGES;
+  uint64_t* xfull = wempty + W_STAGES;   // [KMAX / BK]
+  uint64_t* xempty = xfull + KMAX / BK;  // [KMAX / BK]
+  uint64_t* tfull = xempty + KMAX / BK;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_kb = args.num_kb;  // K16 / 64 <= 4
+  const int tiles_m = args.tiles_m, tiles_n = args.tiles_n;  // beam tiles, sample tiles (units per batch)
+  const int num_units = args.B * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W_STAGES; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+    }
+    for (int s = 0; s < KMAX / BK; ++s) {
+      mbar_init(&xfull[s], CONV_WARPS);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], EPI_WARPS);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer: weight tiles
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int b = u / tiles_n;
+        for (int mt = 0; mt < tiles_m; ++mt) {
+          for (int kb = 0; kb < num_kb; ++kb) {
+            mbar_wait(&wempty[stage], phase ^ 1);
+            uint8_t* st = sW + stage * W_STAGE;
+            mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
+            tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
+            tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+            if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t I256 = idesc_smaj(2 * BB, false);
+      constexpr uint32_t I128 = idesc_smaj(BB, false);
+      constexpr uint32_t I128_NEG = idesc_smaj(BB, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0, ui = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+        const uint32_t xphase = ui & 1;
+        for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+          const int abuf = it & 1;
+          mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_re = tmem_base + abuf * 2 * BB;  // [Re | Im]: 256 columns
+          const uint32_t d_im = d_re + BB;
+          for (int kb = 0; kb < num_kb; ++kb) {
+            if (mt == 0) mbar_wait(&xfull[kb], xphase);  // resident data block converted
+            mbar_wait(&wfull[stage], phase);
+            tc_fence_after();
+            uint8_t* st = sW + stage * W_STAGE;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t krow = kb * BK + kk * 16;
+              const uint64_t xr = desc_x(sX, krow), xi = desc_x(sX + X_PLANE, krow);
+              const uint64_t w_ri = desc_w(st, kk * 32);            // [W_r ; W_i], N = 256
+              const uint64_t w_i = desc_w(st + W_TILE, kk * 32);    // W_i, N = 128
+              const uint64_t w_r = w_ri;                            // W_r, N = 128
+              const uint32_t acc = (kb | kk) ? 1u : 0u;
+              if (TCBF_ABLATE(args, 2)) continue;
+              mma_f16_ss(d_re, xr, w_ri, I256, acc);      // [Re | Im] += X_r [W_r ; W_i]^T
+              mma_f16_ss(d_re, xi, w_i, I128_NEG, 1u);    // Re += -X_i W_i^T
+              mma_f16_ss(d_im, xi, w_r, I128, 1u);        // Im += X_i W_r^T
+            }
+            mma_commit(&wempty[stage]);
+            if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data block
+            if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(&tfull[abuf]);
+        }
+      }
+    }
+  } else if (warp < 2 + EPI_WARPS) {
+    // ------------------------------------------------------------ epilogue: coalesced line stores
+    const int q = warp & 3;                 // TMEM lane quadrant = samples 32q..32q+31 of the tile
+    const int half = (warp - 2) / 4;        // 8 warps: half 0 stores Re, half 1 Im
+    constexpr int SPLIT = EPI_WARPS / 4;
+    constexpr int MY_CHUNKS = 8 / SPLIT;    // 32-column chunks of the 256 accumulator columns
+    const size_t N = (size_t)args.N;
+    const int M = args.M;
+    int it = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const int b = u / tiles_n;
+      const int n = (u - b * tiles_n) * BS + q * 32 + lane;  // this thread's sample
+      const bool n_ok = n < args.N;
+      for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(&tfull[abuf], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BB + half * (8 / SPLIT) * 32;
+        uint32_t v[2][32];
+        tmem_ld_32x32b_x32(tbase, v[0]);
+#pragma unroll
+        for (int i = 0; i < MY_CHUNKS; ++i) {
+          const int ch = half * MY_CHUNKS + i;  // 0..3 Re, 4..7 Im
+          const int part = ch >> 2;
+          const int m0 = mt * BB + (ch & 3) * 32;
+          tmem_wait_ld();
+          if (i + 1 < MY_CHUNKS) {
+            tmem_ld_32x32b_x32(tbase + (i + 1) * 32, v[(i + 1) & 1]);
+          } else {  // all TMEM reads of this tile issued and complete: release the buffer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[abuf]);
+          }
+          const uint32_t* vv = v[i & 1];
+          if (TCBF_ABLATE(args, 1)) continue;
+          if (n_ok) {
+            float* dst = args.out + ((size_t)(2 * b + part) * M + m0) * N + n;
+            if (m0 + 32 <= M) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) dst[(size_t)j * N] = __uint_as_float(vv[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (m0 + j < M) dst[(size_t)j * N] = __uint_as_float(vv[j]);
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ converters: fp32 data -> resident A
+    const int ct = threadIdx.x - SCfg<EPI_WARPS>::CONV0 * 32;  // 0..255
+    constexpr int NT = CONV_WARPS * 32;
+    constexpr int ITEMS = BK * (BS / 8) / NT;  // 16-byte output chunks per thread per K block
+    const int N = args.N;
+    int ui = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+      const int b = u / tiles_n;
+      const int n0 = (u - b * tiles_n) * BS;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        float re[ITEMS][8], im[ITEMS][8];
+        // loads first (all in flight), then wait for the block to be free, then convert + store
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int item = ct + i * NT;
+          const int kr = item / (BS / 8), cc = item % (BS / 8);
+          const int k = kb * BK + kr, n = n0 + cc * 8;
+          if (VEC && LAYOUT == 0 && k < K && n + 8 <= N) {
+            const float4* p = reinterpret_cast<const float4*>(xsrc + (((size_t)b * K + k) * N + n) * 2);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 f = __ldg(p + j);
+              re[i][2 * j] = f.x; im[i][2 * j] = f.y; re[i][2 * j + 1] = f.z; im[i][2 * j + 1] = f.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float a = 0.f, c = 0.f;
+              if (k < K && n + j < N) {
+                if (LAYOUT == 0) {
+                  const float2 f = __ldg(reinterpret_cast<const float2*>(xsrc) + ((size_t)b * K + k) * N + n + j);
+                  a = f.x; c = f.y;
+                } else {
+                  a = __ldg(xsrc + (((size_t)b * 2 + 0) * K + k) * N + n + j);
+                  c = __ldg(xsrc + (((size_t)b * 2 + 1) * K + k) * N + n + j);
+                }
+              }
+              re[i][j] = a; im[i][j] = c;
+            }
+          }
+        }
+        mbar_wait(&xempty[kb], (ui & 1) ^ 1);
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+          const int item = ct + i * NT;
+          const int kr = item / (BS / 8), cc = item % (BS / 8);
+          const int k = kb * BK + kr;
+          const int off = (cc >> 3) * (KMAX * 128) + k * 128 + (((cc & 7) ^ (k & 7)) << 4);
+          *reinterpret_cast<uint4*>(sX + off) = make_uint4(h2u(re[i][0], re[i][1]), h2u(re[i][2], re[i][3]),
+                                                           h2u(re[i][4], re[i][5]), h2u(re[i][6], re[i][7]));
+          *reinterpret_cast<uint4*>(sX + X_PLANE + off) = make_uint4(
+              h2u(im[i][0], im[i][1]), h2u(im[i][2], im[i][3]), h2u(im[i][4], im[i][5]), h2u(im[i][6], im[i][7]));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xfull[kb]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+template <int LAYOUT, bool VEC, int EPI_WARPS>
+cudaError_t launch_smaj(const CUtensorMap& tmW, const GemmF16Args& a, const float* x, int K, int num_sms,
+                        cudaStream_t s) {
+  auto kern = cgemm_f16_smaj_kernel<LAYOUT, VEC, EPI_WARPS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int units = a.B * a.tiles_n;
+  const int grid = units < num_sms ? units : num_sms;
+  kern<<<grid, SCfg<EPI_WARPS>::NUM_THREADS, SMEM_BYTES, s>>>(tmW, a, x, K);
+  return cudaGetLastError();
+}
+
+template <int EPI_WARPS>
+cudaError_t launch_smaj_layout(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
+                               int K, int num_sms, cudaStream_t stream) {
+  const bool vec = layout == 0 && (args.N % 8 == 0) && (reinterpret_cast<uintptr_t>(x_src) % 16 == 0);
+  if (layout == 0)
+    return vec ? launch_smaj<0, true, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream)
+               : launch_smaj<0, false, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream);
+  return launch_smaj<1, false, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream);
+}
+
+}  // namespace
+
+bool gemm_f16_smaj_supported(int64_t K16) { return K16 <= KMAX; }
+
+// args: tiles_m = beam tiles (128), tiles_n = sample tiles (128), num_kb = K16 / 64
+cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
+                                 int K, int epi_warps, int num_sms, cudaStream_t stream) {
+  if (epi_warps == 8) return launch_smaj_layout<8>(tmW, args, x_src, layout, K, num_sms, stream);
+  return launch_smaj_layout<4>(tmW, args, x_src, layout, K, num_sms, stream);
+}
+
+}  // namespace tcbf

@@ -52,6 +52,10 @@ int gemm_f16_conv_block_k();
 int gemm_f16_conv_splits(int tiles, int num_kb, int num_sms);
 cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                  const GemmF16Args& args, int layout, int num_sms, cudaStream_t stream);
+bool gemm_f16_smaj_supported(int64_t K16);
+// sample-major fused kernel (gemm_f16_smaj.cu): tiles_m = beam tiles, tiles_n = 128-sample tiles
+cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
+                                 int K, int epi_warps, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);

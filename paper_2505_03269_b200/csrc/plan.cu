@@ -190,8 +190,16 @@ void choose_kernels(tcbf_plan* p) {
   p->f16_multicast = env_int("TCBF_F16_MC", 1) != 0;
   p->conv_splits_override = env_int("TCBF_CONV_SPLITS", 0);
   p->raw_mode = TCBF_RAW_PACK;
+  // fused kernel kind: sample-major (coalesced line stores straight from TMEM, any N) by default;
+  // the beam-major TMA-store kernel (needs N % 4 == 0) stays selectable for comparison
+  p->f16_fused_kind = TCBF_FUSED_SMAJ;
+  if (const char* e = getenv("TCBF_F16_FUSED"))
+    if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
+  p->smaj_epi_warps = env_int("TCBF_SMAJ_EPI", 8) == 4 ? 4 : 8;
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
-    if (tcbf::gemm_f16_fused_supported(p->kp, p->N)) {
+    const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ ? tcbf::gemm_f16_smaj_supported(p->kp)
+                                                              : tcbf::gemm_f16_fused_supported(p->kp, p->N);
+    if (fusable) {
       p->raw_mode = TCBF_RAW_FUSED;
     } else if (p->M <= 128 && p->N % 4 == 0) {
       // every data element enters one tile: stream the fp32 data through the GEMM once; needs
@@ -438,7 +446,9 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
   switch (entry) {
     case TCBF_ENTRY_BEAMFORM: return gemm_kernel_name(plan);
     case TCBF_ENTRY_BEAMFORM_RAW:
-      if (plan->raw_mode == TCBF_RAW_FUSED) return "f16_tcgen05_fused_pack_bres_128x128";
+      if (plan->raw_mode == TCBF_RAW_FUSED)
+        return plan->f16_fused_kind == TCBF_FUSED_SMAJ ? "f16_tcgen05_fused_smaj_128x128"
+                                                       : "f16_tcgen05_fused_pack_bres_128x128";
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
@@ -498,6 +508,29 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_SMAJ) {
+    // weights as the stacked K-major B operand: box {64 K, 128 beams} per plane, 128-byte swizzle
+    CUtensorMap tw;
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + 127) / 128);   // beam tiles
+    a.tiles_n = (int)((plan->N + 127) / 128);   // 128-sample units per batch entry
+    a.num_kb = (int)(plan->kp / 64);
+    const int64_t nu = (int64_t)a.tiles_n * plan->B;
+    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
+    a.num_tiles = (int)(nu * a.tiles_m);
+    a.out = static_cast<float*>(out);
+    a.debug = plan->debug;
+    cudaError_t e = tcbf::launch_gemm_f16_smaj(tw, a, x_src, (int)layout, (int)plan->K, plan->smaj_epi_warps,
+                                               plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "fused (sample-major) beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
   if (plan->raw_mode == TCBF_RAW_FUSED) {
     CUtensorMap ta, tc;
     s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,

@@ -11,6 +11,7 @@
 
 enum { TCBF_B1K_POPC = 0, TCBF_B1K_I8 = 1, TCBF_B1K_F4 = 4, TCBF_B1K_BMMA = 5 };
 enum { TCBF_RAW_PACK = 0, TCBF_RAW_FUSED = 1, TCBF_RAW_STREAM = 2 };
+enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_BEAM_MAJOR = 1 };
 
 struct tcbf_plan_s {
   int64_t M, N, K, B;
@@ -22,7 +23,9 @@ struct tcbf_plan_s {
   size_t w_bytes, x_bytes, out_bytes;
   // kernel choice (choose_kernels in plan.cu)
   int f16_variant;    // tcbf::F16_V_*
-  int f16_multicast;  // fused kernel: weight tiles multicast across CTA pairs
+  int f16_multicast;  // beam-major fused kernel: weight tiles multicast across CTA pairs
+  int f16_fused_kind; // TCBF_FUSED_*: which fused fp32-data kernel tcbf_beamform_raw runs
+  int smaj_epi_warps; // sample-major fused kernel: epilogue warps (4 or 8)
   int raw_mode;       // TCBF_RAW_*: what tcbf_beamform_raw runs
   int conv_splits_override;  // streaming-conversion K split (0 = by shape)
   int b1_kernel;      // TCBF_B1K_*: fp4 +-1 tensor cores (default), int8 AND form, legacy b1 mma.sync, popc

@@ -48,11 +48,6 @@ def plan_shard(B: int, N: int, rank: int, world: int, align_n: int = 4) -> Shard
     return Shard(0, B, n0, nn, "samples")
 
 
-def weak_shard(B_per_rank: int, rank: int) -> Shard:
-    """Weak scaling (bench.py): every rank owns its own B_per_rank global batch entries."""
-    return Shard(rank * B_per_rank, B_per_rank, 0, -1, "batch")
-
-
 def gather_outputs(local, group=None):
     """Optional output gather (the only data collective): concatenates the
     per-rank [nb,2,M,N] outputs along the batch dimension on every rank.  Requires equal
@@ -81,4 +76,17 @@ def max_over_ranks(value: float, device=None) -> float:
         device = "cpu"
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    """Sum of a scalar over all ranks (e.g. board energy of every GPU of the job)."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    if dist.get_backend() != "nccl":
+        device = "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())

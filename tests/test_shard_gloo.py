@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2505_03269_b200.shard import (contiguous_slice, gather_outputs, max_over_ranks, plan_shard,
-                                         weak_shard)
+                                         sum_over_ranks)
 
 
 def test_contiguous_slices_cover_once():
@@ -34,7 +34,10 @@ def test_plan_shard_modes():
         assert s.mode == "samples" and s.n0 % 4 == 0
         cols += list(range(s.n0, s.n0 + s.nn))
     assert cols == list(range(16384))
-    assert weak_shard(256, 5).b0 == 1280
+    s = plan_shard(8, 256, 5, 8)            # ultrasound 8 frames on 8 GPUs: one each
+    assert (s.mode, s.b0, s.nb) == ("batch", 5, 1)
+    s = plan_shard(8, 256, 2, 3)            # unequal slices: 3, 3, 2
+    assert (s.b0, s.nb) == (6, 2)
 
 
 def _free_port():
@@ -56,8 +59,9 @@ def _worker(rank, world, port, q):
         local = torch.from_numpy(oracle.cgemm_b1(w, x, 0, M, N, K, sh.nb))
         full = gather_outputs(local)
         t = max_over_ranks(float(rank + 1))
+        tot = sum_over_ranks(float(rank + 1))
         if rank == 0:
-            q.put((full.numpy(), t))
+            q.put((full.numpy(), t, tot))
     finally:
         dist.destroy_process_group()
 
@@ -71,7 +75,7 @@ def test_sharded_equals_unsharded_gloo():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    full, tmax = q.get(timeout=120)
+    full, tmax, tsum = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -79,4 +83,4 @@ def test_sharded_equals_unsharded_gloo():
     w = synth.to_interleaved(synth.generate("adc", 77, 0, B, M, K))
     x = synth.to_interleaved(synth.generate("adc", 77, 1, B, K, N))
     assert np.array_equal(full, oracle.cgemm_b1(w, x, 0, M, N, K, B))
-    assert tmax == 2.0
+    assert tmax == 2.0 and tsum == 3.0

@@ -1,0 +1,59 @@
+"""A/B of the fused fp32-data 16-bit kernels on a radio-shaped workload (dev tool, not the bench):
+sample-major (coalesced line stores from TMEM, 8 or 4 epilogue warps) vs the beam-major TMA-store
+kernel, each against pack + beamform (max abs difference and bitwise equality) and CUDA-event timed.
+
+    python tools/ab_fused.py [M N K B] [iters]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2505_03269_b200 as tcbf  # noqa: E402
+import synth  # noqa: E402
+
+VARIANTS = [("smaj8", {}), ("smaj4", {"TCBF_SMAJ_EPI": "4"}), ("beam", {"TCBF_F16_FUSED": "beam"}),
+            ("beam_nomc", {"TCBF_F16_FUSED": "beam", "TCBF_F16_MC": "0"})]
+
+
+def main():
+    a = [int(v) for v in sys.argv[1:5]] if len(sys.argv) >= 5 else [1024, 1024, 256, 256]
+    iters = int(sys.argv[5]) if len(sys.argv) > 5 else 50
+    M, N, K, B = a
+    seed = synth.SEED_BASE + 1
+    w = synth.generate_device("phase", seed, 0, B, M, K)
+    x = synth.generate_device("adc", seed, 1, B, K, N)
+    ref_plan = tcbf.Plan(M, N, K, B, "f16")
+    wp = ref_plan.pack(tcbf.WEIGHTS, w)
+    ref = ref_plan.beamform(wp, ref_plan.pack(tcbf.DATA, x))
+    torch.cuda.synchronize()
+    ops = 8.0 * M * N * K * B
+    byts = B * (4 * M * K + 8 * K * N + 8 * M * N)
+    reps = int(os.environ.get("AB_REPS", "2"))
+    for name, env in VARIANTS * reps:    # interleaved repeats: the board heats up over a run
+        for k in ("TCBF_SMAJ_EPI", "TCBF_F16_FUSED", "TCBF_F16_MC"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        plan = tcbf.Plan(M, N, K, B, "f16")
+        out = plan.alloc_output()
+        plan.beamform_raw(wp, x, out=out)
+        torch.cuda.synchronize()
+        diff = (out - ref).abs().max().item()
+        same = torch.equal(out, ref)
+        for _ in range(5):
+            plan.beamform_raw(wp, x, out=out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            plan.beamform_raw(wp, x, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / iters
+        print(f"{name:10s} {plan.raw_variant:38s} {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TeraOps/s  "
+              f"{byts / ms / 1e6:7.1f} GB/s (fp32-data bytes)  bitwise={same} maxdiff={diff:.3g}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -112,7 +112,7 @@ def misc():
     wsrc = plan.steering_weights(pos, th, fr, 1.0)
     wp = plan.pack(tcbf.WEIGHTS, wsrc)
     _, x = _srcs(M, N, K, B, 5)
-    ref = plan.beamform(wp, plan.pack(tcbf.DATA, _dev(x)))
+    ref = plan.beamform_raw(wp, _dev(x))   # the call tcbf_beamform_host makes per chunk
     xh = torch.from_numpy(x).pin_memory()
     oh = torch.empty(tuple(ref.shape), dtype=ref.dtype).pin_memory()
     plan.beamform_host(wp, xh, oh)
