@@ -89,7 +89,12 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int LAYOUT, bool VEC, int EPI_WARPS>
+
+// MC: CTA pairs (clusters of 2) take adjacent units of the same batch entry and walk the same
+// (beam tile, K block) sequence, so their weight stages are identical: each CTA TMA-loads one of
+// the two planes and multicasts it into both (half the L2 -> SM weight traffic); a stage is
+// refilled only when the MMAs of BOTH CTAs have retired (empty barrier count 2, multicast commit).
+template <int LAYOUT, bool VEC, int EPI_WARPS, bool MC>
 __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     cgemm_f16_smaj_kernel(const __grid_constant__ CUtensorMap tmW, GemmF16Args args, const float* __restrict__ xsrc,
                           int K) {
@@ -110,11 +115,15 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
   const int num_kb = args.num_kb;  // K16 / 64 <= 4
   const int tiles_m = args.tiles_m, tiles_n = args.tiles_n;  // beam tiles, sample tiles (units per batch)
   const int num_units = args.B * tiles_n;
+  // unit walk: single CTAs stride over all units; pairs take units (2p + rank) (units even)
+  const int rank = MC ? (int)cluster_ctarank() : 0;
+  const int u_first = MC ? 2 * (int)(blockIdx.x >> 1) + rank : (int)blockIdx.x;
+  const int u_step = MC ? 2 * (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < W_STAGES; ++s) {
       mbar_init(&wfull[s], 1);
-      mbar_init(&wempty[s], 1);
+      mbar_init(&wempty[s], MC ? 2 : 1);
     }
     for (int s = 0; s < KMAX / BK; ++s) {
       mbar_init(&xfull[s], CONV_WARPS);
@@ -132,7 +141,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     tmem_relinquish();
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // peers signal this CTA's barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -141,15 +150,19 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         for (int mt = 0; mt < tiles_m; ++mt) {
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&wempty[stage], phase ^ 1);
             uint8_t* st = sW + stage * W_STAGE;
             mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
-            tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
-            tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+            if (MC) {
+              tma_load_3d_mc(st + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
+            } else {
+              tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
+              tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+            }
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
         }
@@ -164,7 +177,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0, ui = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+      for (int u = u_first; u < num_units; u += u_step, ++ui) {
         const uint32_t xphase = ui & 1;
         for (int mt = 0; mt < tiles_m; ++mt, ++it) {
           const int abuf = it & 1;
@@ -190,7 +203,8 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
               mma_f16_ss(d_re, xi, w_i, I128_NEG, 1u);    // Re += -X_i W_i^T
               mma_f16_ss(d_im, xi, w_r, I128, 1u);        // Im += X_i W_r^T
             }
-            mma_commit(&wempty[stage]);
+            if (MC) mma_commit_mc(&wempty[stage]);  // the stage is free in both CTAs
+            else mma_commit(&wempty[stage]);
             if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data block
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -207,7 +221,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     const size_t N = (size_t)args.N;
     const int M = args.M;
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = u_first; u < num_units; u += u_step) {
       const int b = u / tiles_n;
       const int n = (u - b * tiles_n) * BS + q * 32 + lane;  // this thread's sample
       const bool n_ok = n < args.N;
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     constexpr int ITEMS = BK * (BS / 8) / NT;  // 16-byte output chunks per thread per K block
     const int N = args.N;
     int ui = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+    for (int u = u_first; u < num_units; u += u_step, ++ui) {
       const int b = u / tiles_n;
       const int n0 = (u - b * tiles_n) * BS;
       for (int kb = 0; kb < num_kb; ++kb) {
@@ -309,33 +323,51 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // no CTA exits while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
 }
 
-template <int LAYOUT, bool VEC, int EPI_WARPS>
+template <int LAYOUT, bool VEC, int EPI_WARPS, bool MC>
 cudaError_t launch_smaj(const CUtensorMap& tmW, const GemmF16Args& a, const float* x, int K, int num_sms,
                         cudaStream_t s) {
-  auto kern = cgemm_f16_smaj_kernel<LAYOUT, VEC, EPI_WARPS>;
+  auto kern = cgemm_f16_smaj_kernel<LAYOUT, VEC, EPI_WARPS, MC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = a.B * a.tiles_n;
-  const int grid = units < num_sms ? units : num_sms;
-  kern<<<grid, SCfg<EPI_WARPS>::NUM_THREADS, SMEM_BYTES, s>>>(tmW, a, x, K);
+  if (!MC) {
+    const int grid = units < num_sms ? units : num_sms;
+    kern<<<grid, SCfg<EPI_WARPS>::NUM_THREADS, SMEM_BYTES, s>>>(tmW, a, x, K);
+    return cudaGetLastError();
+  }
+  const int pairs = units / 2 < num_sms / 2 ? units / 2 : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(SCfg<EPI_WARPS>::NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmW, a, x, K);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-template <int EPI_WARPS>
+template <int EPI_WARPS, bool MC>
 cudaError_t launch_smaj_layout(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
                                int K, int num_sms, cudaStream_t stream) {
   const bool vec = layout == 0 && (args.N % 8 == 0) && (reinterpret_cast<uintptr_t>(x_src) % 16 == 0);
   if (layout == 0)
-    return vec ? launch_smaj<0, true, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream)
-               : launch_smaj<0, false, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream);
-  return launch_smaj<1, false, EPI_WARPS>(tmW, args, x_src, K, num_sms, stream);
+    return vec ? launch_smaj<0, true, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream)
+               : launch_smaj<0, false, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream);
+  return launch_smaj<1, false, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream);
 }
 
 }  // namespace
@@ -344,9 +376,14 @@ bool gemm_f16_smaj_supported(int64_t K16) { return K16 <= KMAX; }
 
 // args: tiles_m = beam tiles (128), tiles_n = sample tiles (128), num_kb = K16 / 64
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
-                                 int K, int epi_warps, int num_sms, cudaStream_t stream) {
-  if (epi_warps == 8) return launch_smaj_layout<8>(tmW, args, x_src, layout, K, num_sms, stream);
-  return launch_smaj_layout<4>(tmW, args, x_src, layout, K, num_sms, stream);
+                                 int K, int epi_warps, bool multicast, int num_sms, cudaStream_t stream) {
+  // weight multicast across CTA pairs needs pairs of units of one batch entry (tiles_n even)
+  const bool mc = multicast && args.tiles_n % 2 == 0 && args.B * args.tiles_n >= 2;
+  if (epi_warps == 4)
+    return mc ? launch_smaj_layout<4, true>(tmW, args, x_src, layout, K, num_sms, stream)
+              : launch_smaj_layout<4, false>(tmW, args, x_src, layout, K, num_sms, stream);
+  return mc ? launch_smaj_layout<8, true>(tmW, args, x_src, layout, K, num_sms, stream)
+            : launch_smaj_layout<8, false>(tmW, args, x_src, layout, K, num_sms, stream);
 }
 
 }  // namespace tcbf

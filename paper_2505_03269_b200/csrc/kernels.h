@@ -24,6 +24,7 @@ struct GemmF16Args {
   int group_m; // tile rows per rasterisation group (tile_coords)
   int splits, kb_per_split;  // K split of the streaming-conversion kernel (fp32 TMA reduce-add)
   unsigned long long* trace;  // TCBF_DEV timeline of the fused kernel (globaltimer stamps), else null
+  int multicast;              // interleaved kernel: weight multicast across CTA pairs (0 = off)
 };
 
 // fp16 GEMM kernel variants (tile N x K-block x stages x epilogue warps)
@@ -55,7 +56,7 @@ cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX,
 bool gemm_f16_smaj_supported(int64_t K16);
 // sample-major fused kernel (gemm_f16_smaj.cu): tiles_m = beam tiles, tiles_n = 128-sample tiles
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
-                                 int K, int epi_warps, int num_sms, cudaStream_t stream);
+                                 int K, int epi_warps, bool multicast, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);

@@ -452,7 +452,7 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
-      return plan->prec == TCBF_PREC_F16 ? "f16_tcgen05_interleaved_128x64" : "none";
+      return plan->prec == TCBF_PREC_F16 ? "f16_tcgen05_interleaved_smaj_64x128" : "none";
   }
   return "none";
 }
@@ -526,7 +526,7 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     a.out = static_cast<float*>(out);
     a.debug = plan->debug;
     cudaError_t e = tcbf::launch_gemm_f16_smaj(tw, a, x_src, (int)layout, (int)plan->K, plan->smaj_epi_warps,
-                                               plan->num_sms, st);
+                                               plan->f16_multicast != 0, plan->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "fused (sample-major) beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;
@@ -657,14 +657,15 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
   s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_f16, 2 * plan->N, plan->K, plan->B, 64, bk,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (s != TCBF_OK) return s;
-  s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
-                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-  if (s != TCBF_OK) return s;
+  memset(&tc, 0, sizeof(tc));  // output written by coalesced st.global straight from TMEM (no TMA map)
   tcbf::GemmF16Args a;
   memset(&a, 0, sizeof(a));
+  a.multicast = plan->f16_multicast;
   a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
   a.tiles_m = (int)((plan->M + 127) / 128);
   a.tiles_n = (int)((plan->N + bnc - 1) / bnc);
+  a.out = static_cast<float*>(out);
+  a.debug = plan->debug;
   const int64_t nt = (int64_t)a.tiles_m * a.tiles_n * plan->B;
   if (nt > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
   a.num_tiles = (int)nt;

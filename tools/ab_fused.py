@@ -13,8 +13,17 @@ import torch  # noqa: E402
 import paper_2505_03269_b200 as tcbf  # noqa: E402
 import synth  # noqa: E402
 
+if os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCBF_DEBUG honoured)
+    from paper_2505_03269_b200 import build as _b
+    tcbf.library_path = _b.build_tcbf(dev=True)
+
 VARIANTS = [("smaj8", {}), ("smaj4", {"TCBF_SMAJ_EPI": "4"}), ("beam", {"TCBF_F16_FUSED": "beam"}),
             ("beam_nomc", {"TCBF_F16_FUSED": "beam", "TCBF_F16_MC": "0"})]
+if os.environ.get("AB_VARIANTS"):   # e.g. "smaj8:,nostore:TCBF_DEBUG=1,nomma:TCBF_DEBUG=2"
+    VARIANTS = []
+    for item in os.environ["AB_VARIANTS"].split(","):
+        name, _, envs = item.partition(":")
+        VARIANTS.append((name, dict(e.split("=") for e in envs.split(";") if e)))
 
 
 def main():
@@ -32,27 +41,35 @@ def main():
     byts = B * (4 * M * K + 8 * K * N + 8 * M * N)
     reps = int(os.environ.get("AB_REPS", "2"))
     for name, env in VARIANTS * reps:    # interleaved repeats: the board heats up over a run
-        for k in ("TCBF_SMAJ_EPI", "TCBF_F16_FUSED", "TCBF_F16_MC"):
+        for k in ("TCBF_SMAJ_EPI", "TCBF_F16_FUSED", "TCBF_F16_MC", "TCBF_DEBUG"):
             os.environ.pop(k, None)
         os.environ.update(env)
         plan = tcbf.Plan(M, N, K, B, "f16")
         out = plan.alloc_output()
-        plan.beamform_raw(wp, x, out=out)
+        f16i = name.startswith("f16i")   # fp16 interleaved data, tcbf_beamform_f16i (NEXT-1)
+        if f16i:
+            xh = x.half()
+            call = lambda: plan.beamform_f16i(wp, xh, out=out)          # noqa: E731
+        else:
+            call = lambda: plan.beamform_raw(wp, x, out=out)            # noqa: E731
+        call()
         torch.cuda.synchronize()
         diff = (out - ref).abs().max().item()
         same = torch.equal(out, ref)
         for _ in range(5):
-            plan.beamform_raw(wp, x, out=out)
+            call()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(iters):
-            plan.beamform_raw(wp, x, out=out)
+            call()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / iters
-        print(f"{name:10s} {plan.raw_variant:38s} {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TeraOps/s  "
-              f"{byts / ms / 1e6:7.1f} GB/s (fp32-data bytes)  bitwise={same} maxdiff={diff:.3g}", flush=True)
+        kname = plan.kernel("f16i") if f16i else plan.raw_variant
+        byts_v = byts - (4 * B * K * N if f16i else 0)   # fp16 data: 4 B per complex sample
+        print(f"{name:10s} {kname:38s} {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TeraOps/s  "
+              f"{byts_v / ms / 1e6:7.1f} GB/s (algorithmic)  bitwise={same} maxdiff={diff:.3g}", flush=True)
 
 
 if __name__ == "__main__":

@@ -66,6 +66,49 @@ __global__ void __launch_bounds__(W * 32, 1) tma_store_warps_kernel(const __grid
     bulk_wait_group<0>();
   }
 }
+// sample-major epilogue pattern (gemm_f16_smaj.cu): unit = (b, 128 samples); per 128-beam tile
+// every thread owns one sample and writes 32 beams per chunk with row stride N: one 128-byte line
+// per warp instruction.  W warps: 4 (one per 32-sample quadrant) or 8 (quadrant x Re/Im half).
+template <int W, int CS>
+__global__ void __launch_bounds__(W * 32, 1) smaj_store_kernel(float* out, int B, int M, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int tiles_n = N / 128, tiles_m = M / 128;
+  const int units = B * tiles_n;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int b = u / tiles_n, n = (u % tiles_n) * 128 + q * 32 + lane;
+    for (int mt = 0; mt < tiles_m; ++mt) {
+#pragma unroll 1
+      for (int ch = half * (8 / (W / 4)); ch < (half + 1) * (8 / (W / 4)); ++ch) {
+        const int part = ch >> 2, m0 = mt * 128 + (ch & 3) * 32;
+        float* dst = out + ((size_t)(2 * b + part) * M + m0) * N + n;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (CS) __stcs(dst + (size_t)j * N, (float)j);
+          else dst[(size_t)j * N] = (float)j;
+        }
+      }
+    }
+  }
+}
+// same tiles, but each warp writes whole 512-byte tile rows with 16-byte stores (what a staged,
+// transposed epilogue would issue): warp w of W handles rows w, w+W, ... of the 256 tile rows
+template <int W>
+__global__ void __launch_bounds__(W * 32, 1) rows_store_kernel(float* out, int B, int M, int N) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_n = N / 128, tiles_m = M / 128;
+  const int units = B * tiles_n;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int b = u / tiles_n, n0 = (u % tiles_n) * 128;
+    for (int mt = 0; mt < tiles_m; ++mt) {
+      for (int r = warp; r < 256; r += W) {
+        const int part = r >> 7, m = mt * 128 + (r & 127);
+        float4* dst = reinterpret_cast<float4*>(out + ((size_t)(2 * b + part) * M + m) * N + n0) + lane;
+        *dst = make_float4(1.f, 2.f, 3.f, (float)r);
+      }
+    }
+  }
+}
 __global__ void vec_store_kernel(float4* out, size_t n4) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
     out[i] = make_float4(1.f, 2.f, 3.f, 4.f);
@@ -112,6 +155,12 @@ int main() {
     return m;
   };
   run("vector float4 stores (grid-stride)", [&] { vec_store_kernel<<<sms * 8, 512>>>((float4*)out, bytes / 16); });
+  run("smaj st.global.f32 lines, 4 warps", [&] { smaj_store_kernel<4, 0><<<sms, 128>>>(out, B, M, N); });
+  run("smaj st.global.f32 lines, 8 warps", [&] { smaj_store_kernel<8, 0><<<sms, 256>>>(out, B, M, N); });
+  run("smaj st.global.cs.f32 lines, 8 warps", [&] { smaj_store_kernel<8, 1><<<sms, 256>>>(out, B, M, N); });
+  run("smaj st.global.f32 lines, 8 warps x 2 CTA/SM", [&] { smaj_store_kernel<8, 0><<<2 * sms, 256>>>(out, B, M, N); });
+  run("tile rows st.global.v4 (512 B), 8 warps", [&] { rows_store_kernel<8><<<sms, 256>>>(out, B, M, N); });
+  run("tile rows st.global.v4 (512 B), 16 warps", [&] { rows_store_kernel<16><<<sms, 512>>>(out, B, M, N); });
   {
     CUtensorMap m = make_map(32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     auto k = tma_store_kernel<128, 32>;
