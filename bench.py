@@ -140,8 +140,15 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
         1.0: "", 2.0: " x2 (int8/fp8 nominal ratio)", 4.0: " x4 (fp4 nominal ratio)"}[ratio]
     if t_hbm >= t_tc:
         ach = byts / t_ms / 1e9
-        return dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
-                    peak_src=peaks["src"], tensor_frac=round(ops / t_ms / 1e12 / tpeak, 4))
+        r = dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
+                 peak_src=peaks["src"], tensor_frac=round(ops / t_ms / 1e12 / tpeak, 4))
+        if fused:
+            # the same launch under SURVEY.md §8(d)'s per-unit bytes as written (data counted at its
+            # packed fp16 size, 4 B per complex sample, although this kernel reads it as fp32)
+            b8 = gemm_bytes(c, False)
+            r["frac_s8d_bytes"] = round(b8 / t_ms / 1e9 / bw, 4)
+            r["s8d_bytes_per_launch"] = b8
+        return r
     ach = ops / t_ms / 1e12
     return dict(bound="tensor", achieved=round(ach, 1), peak=round(tpeak, 1), unit="TOP/s" if ratio > 1 else "TFLOP/s",
                 frac=round(ach / tpeak, 4), peak_src=src, hbm_frac=round(byts / t_ms / 1e9 / bw, 4))
@@ -670,7 +677,8 @@ def main():
                     help="gloo = test mode, all ranks share cuda:0 (production runs use nccl)")
     ap.add_argument("--records", default=None,
                     help="comma-separated extra workloads timed in the same run and reported under 'records' "
-                         "(default for radio_f16: radio_b1,ultrasound_f16 -- both precisions of the metric)")
+                         "(default for radio_f16: radio_b1,ultrasound_f16,radio_f16i -- both precisions of the "
+                         "metric and the NEXT-1 interleaved-fp16 path)")
     ap.add_argument("--no-energy", action="store_true", help="skip the >= 1 s NVML energy loop")
     ap.add_argument("--gather", action="store_true", help="also time the optional NCCL output gather (N > 1)")
     args = ap.parse_args()
@@ -678,7 +686,7 @@ def main():
         args.warmup = 3
     c = CONFIGS[args.config]
     if args.records is None:
-        args.records = "radio_b1,ultrasound_f16" if args.config == "radio_f16" else ""
+        args.records = "radio_b1,ultrasound_f16,radio_f16i" if args.config == "radio_f16" else ""
     if args.impl == "reference":
         return run_reference(args, c)
     return run_tcbf(args, c)

@@ -6,6 +6,6 @@ mkdir -p gpurun_out
 for c in $CFGS; do
   steps=100; [ "$c" = "tiny" ] && steps=2000
   case $c in square_*_16384|ultrasound_f16|square_*_8192) steps=20;; esac
-  timeout 600 python bench.py --config $c --steps $steps --warmup 5 2>gpurun_out/bench_${TAG}_${c}.err | tail -1 > gpurun_out/bench_${TAG}_${c}.json
+  timeout 600 python bench.py --config $c --steps $steps --warmup 5 ${BENCH_FLAGS:---no-cpu-baseline --no-energy} 2>gpurun_out/bench_${TAG}_${c}.err | tail -1 > gpurun_out/bench_${TAG}_${c}.json
   python -c "import json,sys; d=json.load(open('gpurun_out/bench_${TAG}_${c}.json')); r=d['roofline']; print(f\"{d['config']['workload']:18s} {d['value']:9.2f} TOPS  step {d['ms_per_step']:.4f} ms  gemm {d['config']['gemm_ms']:.4f} pack {d['config']['pack_ms']:.4f}  {r['bound']} {r['achieved']} {r['unit']} frac {r['frac']}  e2e {d['e2e']['value']}  cpu {d.get('cpu_baseline',{}).get('value')}  clk {d['clocks'].get('sm_mhz')} {d['clocks'].get('reasons')}\")" 2>&1 | tail -1
 done
