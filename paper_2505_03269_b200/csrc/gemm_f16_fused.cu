@@ -69,21 +69,6 @@ __device__ __forceinline__ uint64_t desc_b_res(const void* plane, uint32_t k_row
   return d;
 }
 
-// timeline stamps (dev only): per CTA 1024 slots; tile it: [4*it + 0..3] = MMA start / MMA issued /
-// epilogue got tile / epilogue done; unit ui: [512 + 4*ui + 0..3] = MMA waits B0 / got B0 /
-// converters got bempty0 / converted block 0
-constexpr int TRACE_SLOTS = 1024;
-__device__ __forceinline__ void stamp(unsigned long long* tr, int slot) {
-#ifdef TCBF_DEV
-  if (tr && slot < TRACE_SLOTS) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    tr[blockIdx.x * TRACE_SLOTS + slot] = t;
-  }
-#else
-  (void)tr; (void)slot;
-#endif
-}
 
 __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   __half2 h = __floats2half2_rn(lo, hi);

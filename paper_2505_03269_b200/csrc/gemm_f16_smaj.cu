@@ -156,12 +156,16 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
           for (int kb = 0; kb < num_kb; ++kb) {
             mbar_wait(&wempty[stage], phase ^ 1);
             uint8_t* st = sW + stage * W_STAGE;
-            mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
-            if (MC) {
-              tma_load_3d_mc(st + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
+            if (TCBF_ABLATE(args, 8) && mt > 0) {  // ablation: weights once per unit (wrong values)
+              mbar_arrive(&wfull[stage]);
             } else {
-              tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
-              tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+              mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
+              if (MC) {
+                tma_load_3d_mc(st + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
+              } else {
+                tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
+                tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+              }
             }
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -181,11 +185,25 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
         const uint32_t xphase = ui & 1;
         for (int mt = 0; mt < tiles_m; ++mt, ++it) {
           const int abuf = it & 1;
+          const unsigned long long tw0 = args.trace ? gtimer() : 0;  // dev timeline (tools/trace_smaj.py)
           mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
+          unsigned long long wwait = 0, xwait = 0;
+          if (args.trace) {
+            stamp(args.trace, 4 * it);
+            stamp_val(args.trace, 512 + 4 * it + 3, gtimer() - tw0);
+          }
           const uint32_t d_re = tmem_base + abuf * 2 * BB;  // [Re | Im]: 256 columns
           const uint32_t d_im = d_re + BB;
           for (int kb = 0; kb < num_kb; ++kb) {
+            if (args.trace) {
+              const unsigned long long a0 = gtimer();
+              if (mt == 0) mbar_wait(&xfull[kb], xphase);
+              const unsigned long long a1 = gtimer();
+              mbar_wait(&wfull[stage], phase);
+              xwait += a1 - a0;
+              wwait += gtimer() - a1;
+            }
             if (mt == 0) mbar_wait(&xfull[kb], xphase);  // resident data block converted
             mbar_wait(&wfull[stage], phase);
             tc_fence_after();
@@ -209,6 +227,11 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
           mma_commit(&tfull[abuf]);
+          if (args.trace) {
+            stamp(args.trace, 4 * it + 1);
+            stamp_val(args.trace, 512 + 4 * it, wwait);
+            stamp_val(args.trace, 512 + 4 * it + 1, xwait);
+          }
         }
       }
     }
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
         const int abuf = it & 1;
         mbar_wait(&tfull[abuf], (it >> 1) & 1);
         tc_fence_after();
+        if (threadIdx.x == 64) stamp(args.trace, 4 * it + 2);
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + abuf * 2 * BB + half * (8 / SPLIT) * 32;
         uint32_t v[2][32];
         tmem_ld_32x32b_x32(tbase, v[0]);
@@ -259,6 +283,10 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
             }
           }
         }
+        if (args.trace && lane == 0) {
+          if (warp == 2) stamp(args.trace, 4 * it + 3);
+          if (warp == 1 + EPI_WARPS) stamp(args.trace, 512 + 4 * it + 2);
+        }
       }
     }
   } else {
@@ -279,7 +307,10 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
           const int item = ct + i * NT;
           const int kr = item / (BS / 8), cc = item % (BS / 8);
           const int k = kb * BK + kr, n = n0 + cc * 8;
-          if (VEC && LAYOUT == 0 && k < K && n + 8 <= N) {
+          if (TCBF_ABLATE(args, 4)) {  // ablation: no data reads (wrong values, timing only)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) re[i][j] = im[i][j] = 0.f;
+          } else if (VEC && LAYOUT == 0 && k < K && n + 8 <= N) {
             const float4* p = reinterpret_cast<const float4*>(xsrc + (((size_t)b * K + k) * N + n) * 2);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {

@@ -525,8 +525,27 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     a.num_tiles = (int)(nu * a.tiles_m);
     a.out = static_cast<float*>(out);
     a.debug = plan->debug;
+#ifdef TCBF_DEV
+    const char* trace_file = getenv("TCBF_TRACE");  // dev timeline (tools/trace_smaj.py)
+    if (trace_file) {
+      cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
+      cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
+    }
+#endif
     cudaError_t e = tcbf::launch_gemm_f16_smaj(tw, a, x_src, (int)layout, (int)plan->K, plan->smaj_epi_warps,
                                                plan->f16_multicast != 0, plan->num_sms, st);
+#ifdef TCBF_DEV
+    if (trace_file) {
+      std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
+      cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(a.trace);
+      if (FILE* f = fopen(trace_file, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
+#endif
     if (e != cudaSuccess) return cuda_fail(e, "fused (sample-major) beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;

@@ -66,7 +66,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+// TMA bulk copy (non-tensor) of `bytes` contiguous global bytes into shared memory, completing on
+// an mbarrier's transaction count (16-byte aligned addresses, size a multiple of 16)
+__device__ __forceinline__ void bulk_load_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// order this thread's generic-proxy global writes before later async-proxy (TMA) reads of them
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
                                             int32_t c0, int32_t c1, int32_t c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -237,6 +248,36 @@ __host__ __device__ constexpr uint32_t idesc_s8(uint32_t M, uint32_t N) {
   return (2u << 4)                 // D format S32
          | (1u << 7) | (1u << 10)  // A, B signed 8-bit
          | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+// timeline stamps (dev only): per CTA 1024 slots; tile it: [4*it + 0..3] = MMA start / MMA issued /
+// epilogue got tile / epilogue done; unit ui: [512 + 4*ui + 0..3] = MMA waits B0 / got B0 /
+// converters got bempty0 / converted block 0
+constexpr int TRACE_SLOTS = 1024;
+__device__ __forceinline__ void stamp(unsigned long long* tr, int slot) {
+#ifdef TCBF_DEV
+  if (tr && slot < TRACE_SLOTS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * TRACE_SLOTS + slot] = t;
+  }
+#else
+  (void)tr; (void)slot;
+#endif
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t = 0;
+#ifdef TCBF_DEV
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#endif
+  return t;
+}
+__device__ __forceinline__ void stamp_val(unsigned long long* tr, int slot, unsigned long long v) {
+#ifdef TCBF_DEV
+  if (tr && slot < TRACE_SLOTS) tr[blockIdx.x * TRACE_SLOTS + slot] = v;
+#else
+  (void)tr; (void)slot; (void)v;
+#endif
 }
 
 }  // namespace tcbf

@@ -5,15 +5,21 @@ kernel, each against pack + beamform (max abs difference and bitwise equality) a
     python tools/ab_fused.py [M N K B] [iters]
 """
 import os
+import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+import bench  # noqa: E402  (ClockSampler: NVML SM clock / power during each variant)
+
 import paper_2505_03269_b200 as tcbf  # noqa: E402
 import synth  # noqa: E402
 
-if os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCBF_DEBUG honoured)
+if os.environ.get("AB_LIB"):       # a specific build (e.g. a compile-time variant under /tmp)
+    tcbf.library_path = os.environ["AB_LIB"]
+elif os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCBF_DEBUG honoured)
     from paper_2505_03269_b200 import build as _b
     tcbf.library_path = _b.build_tcbf(dev=True)
 
@@ -60,16 +66,25 @@ def main():
             call()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        cs = bench.ClockSampler(torch.device("cuda", 0))
+        cs.start()
+        mj0 = cs.energy_mj()
+        t0 = time.perf_counter()
         e0.record()
         for _ in range(iters):
             call()
         e1.record()
         torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        mj1 = cs.energy_mj()
+        cs.stop()
         ms = e0.elapsed_time(e1) / iters
+        clk = statistics.median(cs.samples) if cs.samples else 0
+        watts = (mj1 - mj0) * 1e-3 / wall if (mj0 is not None and mj1 is not None) else 0.0
         kname = plan.kernel("f16i") if f16i else plan.raw_variant
         byts_v = byts - (4 * B * K * N if f16i else 0)   # fp16 data: 4 B per complex sample
         print(f"{name:10s} {kname:38s} {ms * 1e3:8.1f} us  {ops / ms / 1e9:7.1f} TeraOps/s  "
-              f"{byts_v / ms / 1e6:7.1f} GB/s (algorithmic)  bitwise={same} maxdiff={diff:.3g}", flush=True)
+              f"{byts_v / ms / 1e6:7.1f} GB/s (algorithmic)  {clk:5.0f} MHz {watts:5.0f} W  bitwise={same} maxdiff={diff:.3g}", flush=True)
 
 
 if __name__ == "__main__":

@@ -158,6 +158,7 @@ int main() {
   run("smaj st.global.f32 lines, 4 warps", [&] { smaj_store_kernel<4, 0><<<sms, 128>>>(out, B, M, N); });
   run("smaj st.global.f32 lines, 8 warps", [&] { smaj_store_kernel<8, 0><<<sms, 256>>>(out, B, M, N); });
   run("smaj st.global.cs.f32 lines, 8 warps", [&] { smaj_store_kernel<8, 1><<<sms, 256>>>(out, B, M, N); });
+  run("smaj st.global.f32 lines, 16 warps", [&] { smaj_store_kernel<16, 0><<<sms, 512>>>(out, B, M, N); });
   run("smaj st.global.f32 lines, 8 warps x 2 CTA/SM", [&] { smaj_store_kernel<8, 0><<<2 * sms, 256>>>(out, B, M, N); });
   run("tile rows st.global.v4 (512 B), 8 warps", [&] { rows_store_kernel<8><<<sms, 256>>>(out, B, M, N); });
   run("tile rows st.global.v4 (512 B), 16 warps", [&] { rows_store_kernel<16><<<sms, 512>>>(out, B, M, N); });
