@@ -139,15 +139,16 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
     src = peaks["src"] + (" sustained" if long_step else " burst") + {
         1.0: "", 2.0: " x2 (int8/fp8 nominal ratio)", 4.0: " x4 (fp4 nominal ratio)"}[ratio]
     if t_hbm >= t_tc:
-        ach = byts / t_ms / 1e9
+        # achieved = SURVEY.md §8(d)'s per-unit bytes as written (fp16: data counted at its packed
+        # size, 4 B per complex sample, even for the fused kernel that reads it as fp32)
+        b8 = gemm_bytes(c, False)
+        ach = b8 / t_ms / 1e9
         r = dict(bound="hbm", achieved=round(ach, 1), peak=bw, unit="GB/s", frac=round(ach / bw, 4),
                  peak_src=peaks["src"], tensor_frac=round(ops / t_ms / 1e12 / tpeak, 4))
         if fused:
-            # the same launch under SURVEY.md §8(d)'s per-unit bytes as written (data counted at its
-            # packed fp16 size, 4 B per complex sample, although this kernel reads it as fp32)
-            b8 = gemm_bytes(c, False)
-            r["frac_s8d_bytes"] = round(b8 / t_ms / 1e9 / bw, 4)
-            r["s8d_bytes_per_launch"] = b8
+            # the bytes this launch must move (fp32 data read, 8 B per complex sample): context
+            r["frac_kernel_bytes"] = round(byts / t_ms / 1e9 / bw, 4)
+            r["kernel_bytes_per_launch"] = byts
         return r
     ach = ops / t_ms / 1e12
     return dict(bound="tensor", achieved=round(ach, 1), peak=round(tpeak, 1), unit="TOP/s" if ratio > 1 else "TFLOP/s",
@@ -505,7 +506,7 @@ def measure(args, name, c, world, rank, local, dev, steps, warmup, e2e=False, en
     roof["kernel"] = kern
     roof["traffic"] = traffic_for(name, kern) if world == 1 else None
     roof["kernel_ms"] = round(gemm_ms_max, 4)
-    roof["algorithmic_bytes_per_launch"] = gemm_bytes(lc, fused)
+    roof["algorithmic_bytes_per_launch"] = gemm_bytes(lc, False)
     roof["useful_ops_per_launch"] = useful_ops(lc)
     pack_ms_max = max_over_ranks(pack_ms, dev) if not (fused or f16i) else 0.0
     if pack_ms_max > gemm_ms_max:

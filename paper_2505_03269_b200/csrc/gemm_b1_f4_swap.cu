@@ -9,17 +9,29 @@
 //     [D_r^T | D_i^T] += X_r [W_r ; W_i]^T      [D_r^T | D_i^T] += X_i [-W_i ; W_r]^T
 // (the weights' stacked tiles -W_i, W_r, W_i are expanded once per K block; N = 2 TM).
 //
-// Tile = 128 samples x TM beams (TM = 32 or 64); TMEM holds two accumulator buffers of 2 TM
-// columns plus the scale-factor columns, so the epilogue of one tile overlaps the next tile's
-// MMAs.  The epilogue writes the transposed accumulator back as [m][n] rows: each lane holds one
-// sample n, so a warp's 32 lanes write 128 contiguous bytes of one beam row.
+// This shape is a stream of packed data words (N x K bits) against a few weight rows: per
+// 256-bit K block a tile reads 8 KB of packed data and does little MMA work, so what bounds it
+// is how many packed bytes each SM keeps in flight and how cheaply they are expanded.
+//   * packed words arrive by TMA in stages of FOUR K blocks (128-byte rows, 128-byte swizzle so
+//     the expanders' row reads are bank-conflict free), three stages deep: ~120 KB in flight per
+//     SM (was one K block of 32-byte row segments, four deep: 40 KB, latency-bound at ~1360
+//     cycles per K block, 0.22 of the HBM roof);
+//   * the expanded DATA tiles go to TENSOR memory (tcgen05.st, lane = sample, the layout the MMA
+//     reads A from), so shared memory only holds the small weight tiles;
+//   * the weight expansion is spread over four warps (several threads per weight row).
+//
+// Tile = 128 samples x TM beams (TM = 32 or 64).  TMEM: two accumulator buffers of 2 TM columns
+// (the epilogue of one tile overlaps the next tile's MMAs), three expanded-data stages of 64
+// columns (X_r 32 + X_i 32), unit scale factors in the remaining columns.  The epilogue writes the
+// transposed accumulator back as [m][n] rows: each lane holds one sample n, so a warp's 32 lanes
+// write 128 contiguous bytes of one beam row.
 //
 // Roles (persistent CTA per SM):
 //   warp 0        TMEM allocator + single-thread MMA issuer
 //   warps 1-4     epilogue (TMEM lane quarters), 32 x 32 TMA store boxes
-//   warps 5-8     expanders of X_r, X_i (one sample per thread)
-//   warps 9..     expanders of -W_i, W_r, W_i (one beam per thread; TM / 32 warps)
-//   last warp     TMA producer of the packed words
+//   warps 5-8     data expanders (one sample per thread, its TMEM lane), tcgen05.st
+//   warps 9-12    weight expanders (-W_i, W_r, W_i into 128-byte-swizzled smem tiles)
+//   warp 13       TMA producer of the packed words
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -30,35 +42,40 @@
 namespace tcbf {
 namespace {
 
-constexpr int TN = 128;  // samples per tile (MMA M)
-constexpr int KBW = 8;   // 256-bit K blocks -> 128-byte rows of nibbles
+constexpr int TN = 128;   // samples per tile (MMA M)
+constexpr int KBW = 8;    // 256-bit K blocks -> 128-byte rows of nibbles
+constexpr int PKB = 4;    // K blocks per packed TMA stage (128-byte rows of words)
 constexpr int EPI_WARPS = 4;
 constexpr int XEXP_WARPS = 4;
+constexpr int WEXP_WARPS = 4;
+constexpr int NST = 3;    // expanded stages (data in TMEM, weights in smem)
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t SF_COL = 256;
 
 template <int TM>
 struct SwapCfg {
-  static constexpr int X_TILE = TN * 128;                // one expanded data plane
-  static constexpr int W_TILE = TM * 128;                // one expanded weight plane
-  static constexpr int STAGE_BYTES = 2 * X_TILE + 3 * W_TILE;  // X_r, X_i, -W_i, W_r, W_i
-  static constexpr int STAGES = TM == 32 ? 3 : 2;
-  static constexpr int P_PLANE_X = TN * KBW * 4;         // packed words: 128 rows x 32 B
-  static constexpr int P_PLANE_W = TM * KBW * 4;
+  static constexpr int W_TILE = TM * 128;                 // one expanded weight tile
+  static constexpr int STAGE_BYTES = 3 * W_TILE;           // -W_i, W_r, W_i
+  static constexpr int P_PLANE_X = TN * PKB * KBW * 4;     // packed words: 128 rows x 128 B
+  static constexpr int P_PLANE_W = TM * PKB * KBW * 4;
   static constexpr int P_STAGE_BYTES = 2 * P_PLANE_X + 2 * P_PLANE_W;
-  static constexpr int P_STAGES = 4;
+  static constexpr int P_STAGES = TM == 32 ? 3 : 2;
   static constexpr int EPI_BYTES = EPI_WARPS * 2 * 4096;
-  static constexpr int P_OFFSET = STAGES * STAGE_BYTES;
+  static constexpr int P_OFFSET = NST * STAGE_BYTES;
   static constexpr int EPI_OFFSET = P_OFFSET + P_STAGES * P_STAGE_BYTES;
   static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
   static constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
-  static constexpr int WEXP_WARPS = TM / 32;
-  static constexpr int EXP_WARPS = XEXP_WARPS + WEXP_WARPS;
   static constexpr int EXP_WARP0 = 1 + EPI_WARPS;
-  static constexpr int PRODUCER_WARP = EXP_WARP0 + EXP_WARPS;
+  static constexpr int WEXP_WARP0 = EXP_WARP0 + XEXP_WARPS;
+  static constexpr int PRODUCER_WARP = WEXP_WARP0 + WEXP_WARPS;
   static constexpr int NUM_THREADS = (PRODUCER_WARP + 1) * 32;
+  // TMEM columns: accumulators [0, 4 TM), data stages, scale factors
+  static constexpr uint32_t X_COL = 4 * TM;
+  static constexpr uint32_t SF_COL = X_COL + 64 * NST;
+  static constexpr int W_TPR = 128 / TM;                  // weight-expander threads per weight row
+  static constexpr int W_WPT = KBW / W_TPR;               // words per thread per K block
   static_assert(SMEM_BYTES <= 232448, "smem budget");
-  static_assert(2 * TM * 2 <= 256, "two accumulator buffers below the scale-factor columns");
+  static_assert(SF_COL + 64 <= TMEM_COLS, "TMEM budget");
+  static_assert(W_TILE % 1024 == 0, "stacked weight tiles must stay on swizzle-atom boundaries");
 };
 
 template <int J>
@@ -69,32 +86,29 @@ template <int J>
 __device__ __forceinline__ uint32_t nib_neg(uint32_t w) {
   return ((w << (3 - J)) & 0x88888888u) ^ 0x22222222u;  // bit 1 -> 0xA (-1), bit 0 -> 0x2 (+1)
 }
-__device__ __forceinline__ void put(uint8_t* row_base, int row, int q, uint4 v) {
-  *reinterpret_cast<uint4*>(row_base + ((q ^ (row & 7)) << 4)) = v;  // 128-byte swizzle
+__device__ __forceinline__ uint4 pm1(uint32_t w) {
+  return make_uint4(nib_pm1<0>(w), nib_pm1<1>(w), nib_pm1<2>(w), nib_pm1<3>(w));
 }
-__device__ __forceinline__ void expand(uint8_t* row_base, int row, const uint4& lo, const uint4& hi) {
-  const uint32_t w[KBW] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-  for (int q = 0; q < KBW; ++q)
-    put(row_base, row, q, make_uint4(nib_pm1<0>(w[q]), nib_pm1<1>(w[q]), nib_pm1<2>(w[q]), nib_pm1<3>(w[q])));
+__device__ __forceinline__ uint4 neg(uint32_t w) {
+  return make_uint4(nib_neg<0>(w), nib_neg<1>(w), nib_neg<2>(w), nib_neg<3>(w));
 }
-__device__ __forceinline__ void expand_pair(uint8_t* pos_base, uint8_t* neg_base, int row, const uint4& lo,
-                                            const uint4& hi) {
-  const uint32_t w[KBW] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-  for (int q = 0; q < KBW; ++q) {
-    put(pos_base, row, q, make_uint4(nib_pm1<0>(w[q]), nib_pm1<1>(w[q]), nib_pm1<2>(w[q]), nib_pm1<3>(w[q])));
-    put(neg_base, row, q, make_uint4(nib_neg<0>(w[q]), nib_neg<1>(w[q]), nib_neg<2>(w[q]), nib_neg<3>(w[q])));
-  }
+// words 4h..4h+3 of K block j of a row in a packed stage (128-byte rows, 128-byte TMA swizzle)
+__device__ __forceinline__ uint4 packed_chunk(const uint8_t* plane, int row, int j, int h) {
+  return *reinterpret_cast<const uint4*>(plane + row * 128 + (((2 * j + h) ^ (row & 7)) << 4));
 }
-__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+// word q of K block j of a row in a packed stage
+__device__ __forceinline__ uint32_t packed_word(const uint8_t* plane, int row, int j, int q) {
+  const int chunk = (2 * j + (q >> 2)) ^ (row & 7);
+  return *reinterpret_cast<const uint32_t*>(plane + row * 128 + chunk * 16 + (q & 3) * 4);
+}
+__device__ __forceinline__ void mma_mxf4_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(
           d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_same(uint32_t taddr, uint32_t v) {
@@ -104,6 +118,31 @@ __device__ __forceinline__ void tmem_st_same(uint32_t taddr, uint32_t v) {
       "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
       "r"(v)
       : "memory");
+}
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+// one row's 256-bit K block (8 words) as e2m1 +-1 nibbles into 32 TMEM columns of its lane, in
+// logical K order (output word 4q + j <- nib_pm1<j>(word q): the same permutation the smem
+// expansion of the weights applies, so every dot product is unchanged)
+__device__ __forceinline__ void expand_tmem(uint32_t taddr, const uint32_t (&w)[KBW]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t v[16];
+#pragma unroll
+    for (int q = 0; q < KBW / 2; ++q) {
+      v[4 * q] = nib_pm1<0>(w[4 * h + q]);
+      v[4 * q + 1] = nib_pm1<1>(w[4 * h + q]);
+      v[4 * q + 2] = nib_pm1<2>(w[4 * h + q]);
+      v[4 * q + 3] = nib_pm1<3>(w[4 * h + q]);
+    }
+    tmem_st_x16(taddr + 16 * h, v);
+  }
 }
 
 // tile t -> (batch, sample tile, beam tile); beam tiles innermost (the weights stay in L2)
@@ -121,14 +160,14 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
                             const __grid_constant__ CUtensorMap tmC, GemmB1Args p, int tiles_m, int tiles_n,
                             int num_tiles) {
   using C = SwapCfg<TM>;
-  constexpr int STAGES = C::STAGES, P_STAGES = C::P_STAGES;
+  constexpr int P_STAGES = C::P_STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* packed = smem + C::P_OFFSET;
   uint8_t* epi_base = smem + C::EPI_OFFSET;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::BAR_OFFSET);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* pfull = empty_bar + STAGES;
+  uint64_t* empty_bar = full_bar + NST;
+  uint64_t* pfull = empty_bar + NST;
   uint64_t* pempty = pfull + P_STAGES;
   uint64_t* tfull = pempty + P_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -140,13 +179,13 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
   const int two_kpad = 2 * (32 * p.Kw - p.K);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], C::EXP_WARPS);
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full_bar[s], XEXP_WARPS + WEXP_WARPS);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < P_STAGES; ++s) {
       mbar_init(&pfull[s], 1);
-      mbar_init(&pempty[s], C::EXP_WARPS);
+      mbar_init(&pempty[s], XEXP_WARPS + WEXP_WARPS);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -165,10 +204,10 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (warp >= 1 && warp <= EPI_WARPS) {  // unit block scales: every byte of columns 256..511 = 0x7F
+  if (warp >= 1 && warp <= EPI_WARPS) {  // unit block scales: every byte of the scale columns = 0x7F
     const uint32_t lanes = (uint32_t)((warp & 3) * 32) << 16;
 #pragma unroll
-    for (uint32_t c = SF_COL; c < TMEM_COLS; c += 32) tmem_st_same(tmem_base + lanes + c, 0x7F7F7F7Fu);
+    for (uint32_t c = C::SF_COL; c < TMEM_COLS; c += 32) tmem_st_same(tmem_base + lanes + c, 0x7F7F7F7Fu);
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
@@ -181,7 +220,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
       // kind::mxf4 block32: e2m1 A/B, UE8M0 scales, fp32 D, K-major, M = 128 samples, N = 2 TM
       constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * TM) >> 3) << 17) | (1u << 23) |
                                  ((uint32_t)(TN >> 4) << 24);
-      const uint32_t sfa = tmem_base + SF_COL, sfb = tmem_base + SF_COL + 128;
+      const uint32_t sfa = tmem_base + C::SF_COL, sfb = tmem_base + C::SF_COL + 32;
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -193,24 +232,20 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * C::STAGE_BYTES;
-          uint8_t* sXr = st;
-          uint8_t* sXi = st + C::X_TILE;
-          uint8_t* sWn = st + 2 * C::X_TILE;   // -W_i, W_r, W_i: consecutive TM-row tiles
+          uint8_t* sWn = smem + stage * C::STAGE_BYTES;  // -W_i, W_r, W_i: consecutive TM-row tiles
           uint8_t* sWr = sWn + C::W_TILE;
+          const uint32_t xa = tmem_base + C::X_COL + 64 * stage;  // X_r columns, X_i at +32
 #pragma unroll
-          for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements (32 bytes) per MMA
-            const uint32_t off = kk * 32;
-            const uint64_t xr = smem_desc_k128(sXr, off), xi = smem_desc_k128(sXi, off);
-            const uint64_t w_ri = smem_desc_k128(sWr, off);  // [W_r; W_i]
-            const uint64_t w_nr = smem_desc_k128(sWn, off);  // [-W_i; W_r]
+          for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements = 32 bytes = 8 TMEM columns per MMA
+            const uint64_t w_ri = smem_desc_k128(sWr, kk * 32);  // [W_r; W_i]
+            const uint64_t w_nr = smem_desc_k128(sWn, kk * 32);  // [-W_i; W_r]
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             if (TCBF_ABLATE(p, 2)) continue;
-            mma_mxf4(d, xr, w_ri, IDESC, sfa, sfb, acc);
-            mma_mxf4(d, xi, w_nr, IDESC, sfa, sfb, 1u);
+            mma_mxf4_ts(d, xa + kk * 8, w_ri, IDESC, sfa, sfb, acc);
+            mma_mxf4_ts(d, xa + 32 + kk * 8, w_nr, IDESC, sfa, sfb, 1u);
           }
           mma_commit(&empty_bar[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[abuf]);
       }
@@ -275,42 +310,79 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
       if (lane == 0) bulk_wait_group<0>();
       __syncwarp();
     }
-  } else if (warp < C::PRODUCER_WARP) {
-    // ------------------------------------------------------------ expanders
-    const int e = threadIdx.x - C::EXP_WARP0 * 32;
-    const bool x_side = e < TN;
-    const int row = x_side ? e : e - TN;
+  } else if (warp < C::WEXP_WARP0) {
+    // ------------------------------------------------------------ data expanders -> TMEM (lane = sample)
+    const int row = 32 * (warp & 3) + lane;  // a warp may only write its TMEM lane quarter
+    const uint32_t lanes = (uint32_t)(32 * (warp & 3)) << 16;
     int stage = 0, ps = 0;
     uint32_t phase = 0, pph = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb0 = 0; kb0 < num_kb; kb0 += PKB) {
         mbar_wait(&pfull[ps], pph);
         const uint8_t* pk = packed + ps * C::P_STAGE_BYTES;
-        const uint8_t* pr = x_side ? pk + row * 32 : pk + 2 * C::P_PLANE_X + row * 32;
-        const int plane = x_side ? C::P_PLANE_X : C::P_PLANE_W;
-        const uint4 r0 = *reinterpret_cast<const uint4*>(pr);
-        const uint4 r1 = *reinterpret_cast<const uint4*>(pr + 16);
-        const uint4 i0 = *reinterpret_cast<const uint4*>(pr + plane);
-        const uint4 i1 = *reinterpret_cast<const uint4*>(pr + plane + 16);
-        mbar_wait(&empty_bar[stage], phase ^ 1);
-        uint8_t* st = smem + stage * C::STAGE_BYTES;
-        if (!(TCBF_ABLATE(p, 4))) {
-          if (x_side) {
-            expand(st + row * 128, row, r0, r1);
-            expand(st + C::X_TILE + row * 128, row, i0, i1);
+        const int nj = min(PKB, num_kb - kb0);
+        for (int j = 0; j < nj; ++j) {
+          const uint4 r0 = packed_chunk(pk, row, j, 0), r1 = packed_chunk(pk, row, j, 1);
+          const uint4 i0 = packed_chunk(pk + C::P_PLANE_X, row, j, 0), i1 = packed_chunk(pk + C::P_PLANE_X, row, j, 1);
+          const uint32_t wr[KBW] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+          const uint32_t wi[KBW] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          tc_fence_after();
+          const uint32_t ta = tmem_base + lanes + C::X_COL + 64 * stage;
+          if (!(TCBF_ABLATE(p, 4))) {
+            expand_tmem(ta, wr);
+            expand_tmem(ta + 32, wi);
           } else {
-            uint8_t* wn = st + 2 * C::X_TILE;
-            expand(wn + C::W_TILE + row * 128, row, r0, r1);                          // W_r
-            expand_pair(wn + 2 * C::W_TILE + row * 128, wn + row * 128, row, i0, i1);  // W_i, -W_i
+            asm volatile("" ::"r"(wr[0]), "r"(wi[0]));
           }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_bar[stage]);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&full_bar[stage]);
-          mbar_arrive(&pempty[ps]);
+        if (lane == 0) mbar_arrive(&pempty[ps]);
+        if (++ps == P_STAGES) { ps = 0; pph ^= 1; }
+      }
+    }
+  } else if (warp < C::PRODUCER_WARP) {
+    // ------------------------------------------------------------ weight expanders -> smem (-W_i, W_r, W_i)
+    const int e = threadIdx.x - C::WEXP_WARP0 * 32;  // 0..127
+    const int row = e / C::W_TPR;
+    const int q0 = (e % C::W_TPR) * C::W_WPT;        // first word of the K block this thread expands
+    int stage = 0, ps = 0;
+    uint32_t phase = 0, pph = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb0 = 0; kb0 < num_kb; kb0 += PKB) {
+        mbar_wait(&pfull[ps], pph);
+        const uint8_t* pw = packed + ps * C::P_STAGE_BYTES + 2 * C::P_PLANE_X;
+        const int nj = min(PKB, num_kb - kb0);
+        for (int j = 0; j < nj; ++j) {
+          uint32_t wr[C::W_WPT], wi[C::W_WPT];
+#pragma unroll
+          for (int qq = 0; qq < C::W_WPT; ++qq) {
+            wr[qq] = packed_word(pw, row, j, q0 + qq);
+            wi[qq] = packed_word(pw + C::P_PLANE_W, row, j, q0 + qq);
+          }
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* wn = smem + stage * C::STAGE_BYTES;  // -W_i
+          if (!(TCBF_ABLATE(p, 4))) {
+#pragma unroll
+            for (int qq = 0; qq < C::W_WPT; ++qq) {
+              const int pos = ((q0 + qq) ^ (row & 7)) << 4;  // 128-byte swizzle of the 16-byte chunk
+              *reinterpret_cast<uint4*>(wn + row * 128 + pos) = neg(wi[qq]);
+              *reinterpret_cast<uint4*>(wn + C::W_TILE + row * 128 + pos) = pm1(wr[qq]);
+              *reinterpret_cast<uint4*>(wn + 2 * C::W_TILE + row * 128 + pos) = pm1(wi[qq]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full_bar[stage]);
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[ps]);
         if (++ps == P_STAGES) { ps = 0; pph ^= 1; }
       }
     }
@@ -322,14 +394,14 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int b, nt, mt;
         swap_coords(t, tiles_m, tiles_n, b, nt, mt);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb0 = 0; kb0 < num_kb; kb0 += PKB) {
           mbar_wait(&pempty[ps], pph ^ 1);
           uint8_t* dst = packed + ps * C::P_STAGE_BYTES;
-          mbar_arrive_expect_tx(&pfull[ps], C::P_STAGE_BYTES);
-          tma_load_3d(dst, &tmX, &pfull[ps], kb * KBW, nt * TN, 2 * b);
-          tma_load_3d(dst + C::P_PLANE_X, &tmX, &pfull[ps], kb * KBW, nt * TN, 2 * b + 1);
-          tma_load_3d(dst + 2 * C::P_PLANE_X, &tmW, &pfull[ps], kb * KBW, mt * TM, 2 * b);
-          tma_load_3d(dst + 2 * C::P_PLANE_X + C::P_PLANE_W, &tmW, &pfull[ps], kb * KBW, mt * TM, 2 * b + 1);
+          mbar_arrive_expect_tx(&pfull[ps], C::P_STAGE_BYTES);  // words past Kw are zero-filled
+          tma_load_3d(dst, &tmX, &pfull[ps], kb0 * KBW, nt * TN, 2 * b);
+          tma_load_3d(dst + C::P_PLANE_X, &tmX, &pfull[ps], kb0 * KBW, nt * TN, 2 * b + 1);
+          tma_load_3d(dst + 2 * C::P_PLANE_X, &tmW, &pfull[ps], kb0 * KBW, mt * TM, 2 * b);
+          tma_load_3d(dst + 2 * C::P_PLANE_X + C::P_PLANE_W, &tmW, &pfull[ps], kb0 * KBW, mt * TM, 2 * b + 1);
           if (++ps == P_STAGES) { ps = 0; pph ^= 1; }
         }
       }
@@ -362,7 +434,10 @@ cudaError_t launch_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CU
 }  // namespace
 
 int gemm_b1_f4_swap_beams(int64_t M) { return M <= 32 ? 32 : (M <= 64 ? 64 : 0); }
+int gemm_b1_f4_swap_box_words() { return PKB * KBW; }
 
+// tensor maps: packed words [2B][rows][Kw] u32, box {32 words, 128 samples} (data) and
+// {32 words, TM beams} (weights), 128-byte swizzle, zero fill past Kw
 cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                                    const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream) {
   if (gemm_b1_f4_swap_beams(args.M) == 32)

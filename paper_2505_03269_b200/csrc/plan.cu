@@ -328,12 +328,14 @@ tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void*
     memset(&tc, 0, sizeof(tc));
     if (plan->b1_swap_beams) {  // few beams: samples on the 128-row MMA dimension, beams on N
       CUtensorMap tw, tx;
-      const uint32_t kbw = (uint32_t)tcbf::gemm_b1_f4_block_words();
-      s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, kbw,
-                    (uint32_t)plan->b1_swap_beams, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      // packed words in boxes of four 256-bit K blocks (128-byte rows, 128-byte swizzle; words past
+      // Kw are zero-filled and never expanded)
+      const uint32_t bw = (uint32_t)tcbf::gemm_b1_f4_swap_box_words();
+      s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B, bw,
+                    (uint32_t)plan->b1_swap_beams, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
       if (s != TCBF_OK) return s;
-      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, kbw, 128,
-                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B, bw, 128,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
       if (s != TCBF_OK) return s;
       if (tma_store) {  // 32 beams x 32 samples boxes, unswizzled 128-byte rows
         s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_INT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 32,
