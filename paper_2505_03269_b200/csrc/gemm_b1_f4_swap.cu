@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (it == 0 && kb < 128) stamp(p.trace, kb);  // dev timeline: MMA got stage kb
           uint8_t* sWn = smem + stage * C::STAGE_BYTES;  // -W_i, W_r, W_i: consecutive TM-row tiles
           uint8_t* sWr = sWn + C::W_TILE;
           const uint32_t xa = tmem_base + C::X_COL + 64 * stage;  // X_r columns, X_i at +32
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[abuf]);
+        if (it == 0) stamp(p.trace, 1000);
       }
     }
   } else if (warp <= EPI_WARPS) {
@@ -319,6 +321,8 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       for (int kb0 = 0; kb0 < num_kb; kb0 += PKB) {
         mbar_wait(&pfull[ps], pph);
+        const bool tr = p.trace && warp == C::EXP_WARP0 && lane == 0 && t == (int)blockIdx.x && kb0 < 128;
+        if (tr) stamp(p.trace, 128 + kb0 / PKB);
         const uint8_t* pk = packed + ps * C::P_STAGE_BYTES;
         const int nj = min(PKB, num_kb - kb0);
         for (int j = 0; j < nj; ++j) {
@@ -327,6 +331,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
           const uint32_t wr[KBW] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
           const uint32_t wi[KBW] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (tr) stamp(p.trace, 256 + kb0 + j);
           tc_fence_after();
           const uint32_t ta = tmem_base + lanes + C::X_COL + 64 * stage;
           if (!(TCBF_ABLATE(p, 4))) {
@@ -339,6 +344,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&full_bar[stage]);
+          if (tr) stamp(p.trace, 384 + kb0 + j);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         __syncwarp();
@@ -379,6 +385,8 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) mbar_arrive(&full_bar[stage]);
+          if (p.trace && warp == C::WEXP_WARP0 && lane == 0 && t == (int)blockIdx.x && kb0 + j < 128)
+            stamp(p.trace, 640 + kb0 + j);
           if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         __syncwarp();
@@ -396,6 +404,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
         swap_coords(t, tiles_m, tiles_n, b, nt, mt);
         for (int kb0 = 0; kb0 < num_kb; kb0 += PKB) {
           mbar_wait(&pempty[ps], pph ^ 1);
+          if (t == (int)blockIdx.x && kb0 < 128) stamp(p.trace, 512 + kb0 / PKB);
           uint8_t* dst = packed + ps * C::P_STAGE_BYTES;
           mbar_arrive_expect_tx(&pfull[ps], C::P_STAGE_BYTES);  // words past Kw are zero-filled
           tma_load_3d(dst, &tmX, &pfull[ps], kb0 * KBW, nt * TN, 2 * b);

@@ -90,11 +90,12 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
 }
 
 
-// MC: CTA pairs (clusters of 2) take adjacent units of the same batch entry and walk the same
-// (beam tile, K block) sequence, so their weight stages are identical: each CTA TMA-loads one of
-// the two planes and multicasts it into both (half the L2 -> SM weight traffic); a stage is
-// refilled only when the MMAs of BOTH CTAs have retired (empty barrier count 2, multicast commit).
-template <int LAYOUT, bool VEC, int EPI_WARPS, bool MC>
+// CL > 1: clusters of CL CTAs take adjacent units of the same batch entry and walk the same
+// (beam tile, K block) sequence, so their weight stages are identical: each CTA TMA-loads 1/CL of
+// the stage (64-row boxes) and multicasts it into all CL CTAs (1/CL of the L2 -> SM weight reads);
+// a stage is refilled only when the MMAs of every CTA of the cluster have retired (empty barrier
+// count CL, multicast commit).
+template <int LAYOUT, bool VEC, int EPI_WARPS, int CL>
 __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
     cgemm_f16_smaj_kernel(const __grid_constant__ CUtensorMap tmW, GemmF16Args args, const float* __restrict__ xsrc,
                           int K) {
@@ -115,15 +116,17 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
   const int num_kb = args.num_kb;  // K16 / 64 <= 4
   const int tiles_m = args.tiles_m, tiles_n = args.tiles_n;  // beam tiles, sample tiles (units per batch)
   const int num_units = args.B * tiles_n;
-  // unit walk: single CTAs stride over all units; pairs take units (2p + rank) (units even)
+  // unit walk: single CTAs stride over all units; clusters take units (CL c + rank) (tiles_n % CL == 0)
+  constexpr bool MC = CL > 1;
+  constexpr uint16_t CL_MASK = (uint16_t)((1u << CL) - 1u);
   const int rank = MC ? (int)cluster_ctarank() : 0;
-  const int u_first = MC ? 2 * (int)(blockIdx.x >> 1) + rank : (int)blockIdx.x;
-  const int u_step = MC ? 2 * (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int u_first = MC ? CL * (int)(blockIdx.x / CL) + rank : (int)blockIdx.x;
+  const int u_step = MC ? CL * (int)(gridDim.x / CL) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < W_STAGES; ++s) {
       mbar_init(&wfull[s], 1);
-      mbar_init(&wempty[s], MC ? 2 : 1);
+      mbar_init(&wempty[s], CL);
     }
     for (int s = 0; s < KMAX / BK; ++s) {
       mbar_init(&xfull[s], CONV_WARPS);
@@ -160,11 +163,14 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
               mbar_arrive(&wfull[stage]);
             } else {
               mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
-              if (MC) {
-                tma_load_3d_mc(st + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
-              } else {
-                tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
-                tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+              // the stage = 4 boxes of 64 beam rows (plane p = box >> 1, rows 64 (box & 1));
+              // CTA `rank` of a cluster of CL loads boxes rank * 4/CL .. and multicasts them
+#pragma unroll
+              for (int bx = rank * (4 / CL); bx < (rank + 1) * (4 / CL); ++bx) {
+                uint8_t* dst = st + (bx >> 1) * W_TILE + (bx & 1) * (W_TILE / 2);
+                if (MC) tma_load_3d_mc(dst, &tmW, &wfull[stage], kb * BK, mt * BB + (bx & 1) * 64, 2 * b + (bx >> 1),
+                                       CL_MASK);
+                else tma_load_3d(dst, &tmW, &wfull[stage], kb * BK, mt * BB + (bx & 1) * 64, 2 * b + (bx >> 1));
               }
             }
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
               mma_f16_ss(d_re, xi, w_i, I128_NEG, 1u);    // Re += -X_i W_i^T
               mma_f16_ss(d_im, xi, w_r, I128, 1u);        // Im += X_i W_r^T
             }
-            if (MC) mma_commit_mc(&wempty[stage]);  // the stage is free in both CTAs
+            if (MC) mma_commit_mc(&wempty[stage], CL_MASK);  // the stage is free in every CTA of the cluster
             else mma_commit(&wempty[stage]);
             if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data block
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
@@ -361,27 +367,28 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
   }
 }
 
-template <int LAYOUT, bool VEC, int EPI_WARPS, bool MC>
+template <int LAYOUT, bool VEC, int CL>
 cudaError_t launch_smaj(const CUtensorMap& tmW, const GemmF16Args& a, const float* x, int K, int num_sms,
                         cudaStream_t s) {
-  auto kern = cgemm_f16_smaj_kernel<LAYOUT, VEC, EPI_WARPS, MC>;
+  constexpr int EPI = 8;
+  auto kern = cgemm_f16_smaj_kernel<LAYOUT, VEC, EPI, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = a.B * a.tiles_n;
-  if (!MC) {
+  if (CL == 1) {
     const int grid = units < num_sms ? units : num_sms;
-    kern<<<grid, SCfg<EPI_WARPS>::NUM_THREADS, SMEM_BYTES, s>>>(tmW, a, x, K);
+    kern<<<grid, SCfg<EPI>::NUM_THREADS, SMEM_BYTES, s>>>(tmW, a, x, K);
     return cudaGetLastError();
   }
-  const int pairs = units / 2 < num_sms / 2 ? units / 2 : num_sms / 2;
+  const int clusters = units / CL < num_sms / CL ? units / CL : num_sms / CL;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(SCfg<EPI_WARPS>::NUM_THREADS);
+  cfg.gridDim = dim3(CL * clusters);
+  cfg.blockDim = dim3(SCfg<EPI>::NUM_THREADS);
   cfg.dynamicSmemBytes = SMEM_BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -391,30 +398,32 @@ cudaError_t launch_smaj(const CUtensorMap& tmW, const GemmF16Args& a, const floa
   return cudaGetLastError();
 }
 
-template <int EPI_WARPS, bool MC>
+template <int CL>
 cudaError_t launch_smaj_layout(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
                                int K, int num_sms, cudaStream_t stream) {
   const bool vec = layout == 0 && (args.N % 8 == 0) && (reinterpret_cast<uintptr_t>(x_src) % 16 == 0);
   if (layout == 0)
-    return vec ? launch_smaj<0, true, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream)
-               : launch_smaj<0, false, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream);
-  return launch_smaj<1, false, EPI_WARPS, MC>(tmW, args, x_src, K, num_sms, stream);
+    return vec ? launch_smaj<0, true, CL>(tmW, args, x_src, K, num_sms, stream)
+               : launch_smaj<0, false, CL>(tmW, args, x_src, K, num_sms, stream);
+  return launch_smaj<1, false, CL>(tmW, args, x_src, K, num_sms, stream);
 }
 
 }  // namespace
 
 bool gemm_f16_smaj_supported(int64_t K16) { return K16 <= KMAX; }
 
-// args: tiles_m = beam tiles (128), tiles_n = sample tiles (128), num_kb = K16 / 64
+// args: tiles_m = beam tiles (128), tiles_n = sample tiles (128), num_kb = K16 / 64; weights
+// tensor map: box {64 K, 64 beam rows} per plane, 128-byte swizzle.  cluster = weight-multicast
+// cluster size (2 = CTA pairs when tiles_n is even, else 1).
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
-                                 int K, int epi_warps, bool multicast, int num_sms, cudaStream_t stream) {
-  // weight multicast across CTA pairs needs pairs of units of one batch entry (tiles_n even)
-  const bool mc = multicast && args.tiles_n % 2 == 0 && args.B * args.tiles_n >= 2;
-  if (epi_warps == 4)
-    return mc ? launch_smaj_layout<4, true>(tmW, args, x_src, layout, K, num_sms, stream)
-              : launch_smaj_layout<4, false>(tmW, args, x_src, layout, K, num_sms, stream);
-  return mc ? launch_smaj_layout<8, true>(tmW, args, x_src, layout, K, num_sms, stream)
-            : launch_smaj_layout<8, false>(tmW, args, x_src, layout, K, num_sms, stream);
+                                 int K, int cluster, int num_sms, cudaStream_t stream) {
+  // (clusters of 4 were measured 1.5x slower on radio fp16 -- 0.99 vs 0.67 ms: co-scheduling 4-CTA
+  // clusters and lock-stepping them costs more than the halved L2 weight reads save -- so the
+  // kernel is built for pairs only)
+  const int units = args.B * args.tiles_n;
+  if (cluster >= 2 && args.tiles_n % 2 == 0 && units >= 2)
+    return launch_smaj_layout<2>(tmW, args, x_src, layout, K, num_sms, stream);
+  return launch_smaj_layout<1>(tmW, args, x_src, layout, K, num_sms, stream);
 }
 
 }  // namespace tcbf

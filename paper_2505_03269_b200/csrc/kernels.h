@@ -56,7 +56,7 @@ cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX,
 bool gemm_f16_smaj_supported(int64_t K16);
 // sample-major fused kernel (gemm_f16_smaj.cu): tiles_m = beam tiles, tiles_n = 128-sample tiles
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
-                                 int K, int epi_warps, bool multicast, int num_sms, cudaStream_t stream);
+                                 int K, int cluster, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);
@@ -70,6 +70,7 @@ struct GemmB1Args {
   int group_m;  // tile rows per rasterisation group (tile_coords)
   int splits;   // split-K factor (int8 kernel): >1 accumulates exact int32 partials with TMA reduce-add
   int kb_per_split;
+  unsigned long long* trace;  // TCBF_DEV timeline (globaltimer stamps) of the swapped kernel, else null
 };
 cudaError_t launch_gemm_b1_popc(const GemmB1Args& args, cudaStream_t stream);
 cudaError_t launch_gemm_b1_mma(const GemmB1Args& args, cudaStream_t stream);  // legacy mma.sync b1 AND

@@ -12,6 +12,9 @@
 //   5  tcgen05.mma kind::mxf4  M=128 N=256 K=64, block32 unit scales, fp32 accumulate
 //   6  tcgen05.mma kind::f16   M=128 N=64  K=16, A from TMEM (the data-in-TMEM fused variant)
 //   7  tcgen05.mma kind::f16   M=128 N=128 K=16, both operands from smem (the fused kernel's MMA)
+//   8  tcgen05.mma kind::mxf4  M=128 N=64  K=64, A from TMEM (the swapped small-M 1-bit kernel, TM=32)
+//   9  tcgen05.mma kind::mxf4  M=128 N=64  K=64, both operands from smem
+//  10  tcgen05.mma kind::mxf4  M=128 N=128 K=64, A from TMEM (swapped kernel, TM=64)
 // Ops are counted as 2 per multiply-accumulate (binary MACs for kinds 0-2).  Host entry point:
 // tcbf_peak_run (extern "C"), timed with CUDA events around one launch after a warm-up launch.
 // This library is a measurement tool: it is not on the beamforming path.
@@ -105,13 +108,20 @@ __device__ __forceinline__ void tmem_st_same(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void mma_mxf4_ts_peak(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], 1;" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(sfa), "r"(sfb)
+      : "memory");
+}
 __device__ __forceinline__ void mma_f16_ts_peak(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc) {
   asm volatile("tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, 1;" ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc),
                "r"(idesc)
                : "memory");
 }
 
-template <int KIND>  // 3 f16, 4 i8, 5 mxf4, 6 f16 A-in-TMEM N=64, 7 f16 N=128
+template <int KIND>  // 3 f16, 4 i8, 5 mxf4, 6 f16 A-in-TMEM N=64, 7 f16 N=128, 8-10 mxf4 N=64/128
 __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -128,7 +138,7 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
     h ^= h >> 15;
     h *= 0x2C1B3C6Du;
     h ^= h >> 13;
-    if (KIND == 3 || KIND >= 6) h &= 0xBBFFBBFFu;  // clear exponent MSB -> |x| < 2 in both halves
+    if (KIND == 3 || KIND == 6 || KIND == 7) h &= 0xBBFFBBFFu;  // clear exponent MSB -> |x| < 2 in both halves
     reinterpret_cast<uint32_t*>(smem)[i] = h;
   }
   if (threadIdx.x == 0) {
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (KIND == 5) {  // unit UE8M0 block scales in columns 256..511
+  if (KIND == 5 || KIND >= 8) {  // unit UE8M0 block scales in columns 256..511
     const uint32_t lanes = (uint32_t)(warp * 32) << 16;
     for (uint32_t c = 256; c < 512; c += 32) tmem_st_same(tmem + lanes + c, 0x7F7F7F7Fu);
     tc_fence_before();
@@ -158,7 +168,8 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
     else if (KIND == 6) idesc = idesc_f16(128, 64, false);
     else if (KIND == 7) idesc = idesc_f16(128, 128, false);
     else if (KIND == 4) idesc = idesc_s8(128, 256);
-    else idesc = (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | (1u << 23) | ((128u >> 4) << 24);
+    else idesc = (1u << 7) | (1u << 10) | (((KIND == 8 || KIND == 9 ? 64u : KIND == 10 ? 128u : 256u) >> 3) << 17) |
+                 (1u << 23) | ((128u >> 4) << 24);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte row
@@ -166,6 +177,8 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
         if (KIND == 3 || KIND == 7) mma_f16_ss(tmem, ad, bd, idesc, 1u);
         else if (KIND == 6) mma_f16_ts_peak(tmem + 256, tmem + kk * 8, bd, idesc);  // A: columns 0..31
         else if (KIND == 4) mma_i8_ss(tmem, ad, bd, idesc, 1u);
+        else if (KIND == 8 || KIND == 10) mma_mxf4_ts_peak(tmem + 128, tmem + kk * 8, bd, idesc, tmem + 256, tmem + 256 + 128);
+        else if (KIND == 9) mma_mxf4_peak(tmem + 128, ad, bd, idesc, tmem + 256, tmem + 256 + 128);
         else mma_mxf4_peak(tmem, ad, bd, idesc, tmem + 256, tmem + 256 + 128);
       }
     }
@@ -199,7 +212,7 @@ extern "C" {
 // -1 for an unknown kind or iters <= 0, else the cudaError_t value.
 __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, double* seconds, double* ops) {
   using namespace tcbf;
-  if (kind < 0 || kind > 7 || iters <= 0 || !seconds || !ops) return -1;
+  if (kind < 0 || kind > 10 || iters <= 0 || !seconds || !ops) return -1;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -226,12 +239,13 @@ __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, do
       work = 2.0 * 32 * 4 * POPC_CHAINS * (double)iters * blocks * threads;
     } else {
       auto k = kind == 3 ? peak_tc_kernel<3> : kind == 4 ? peak_tc_kernel<4> : kind == 5 ? peak_tc_kernel<5>
-             : kind == 6 ? peak_tc_kernel<6> : peak_tc_kernel<7>;
+             : kind == 6 ? peak_tc_kernel<6> : kind == 7 ? peak_tc_kernel<7> : kind == 8 ? peak_tc_kernel<8>
+             : kind == 9 ? peak_tc_kernel<9> : peak_tc_kernel<10>;
       cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
       if (a != cudaSuccess) return a;
       k<<<sms, 128, TC_SMEM>>>(iters, sink);
-      const double kdim = (kind == 3 || kind >= 6) ? 16 : kind == 4 ? 32 : 64;
-      const double ndim = kind == 6 ? 64 : kind == 7 ? 128 : 256;
+      const double kdim = (kind == 3 || kind == 6 || kind == 7) ? 16 : kind == 4 ? 32 : 64;
+      const double ndim = (kind == 6 || kind == 8 || kind == 9) ? 64 : (kind == 7 || kind == 10) ? 128 : 256;
       work = 2.0 * 128 * ndim * kdim * 4 * (double)iters * sms;
     }
     return cudaGetLastError();

@@ -195,7 +195,8 @@ void choose_kernels(tcbf_plan* p) {
   p->f16_fused_kind = TCBF_FUSED_SMAJ;
   if (const char* e = getenv("TCBF_F16_FUSED"))
     if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
-  p->smaj_epi_warps = env_int("TCBF_SMAJ_EPI", 8) == 4 ? 4 : 8;
+  // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
+  p->smaj_cluster = p->f16_multicast ? 2 : 1;
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
     const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ ? tcbf::gemm_f16_smaj_supported(p->kp)
                                                               : tcbf::gemm_f16_fused_supported(p->kp, p->N);
@@ -342,7 +343,26 @@ tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void*
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
         if (s != TCBF_OK) return s;
       }
+#ifdef TCBF_DEV
+      const char* trace_file = getenv("TCBF_TRACE");  // dev timeline (tools/trace_swap.py)
+      if (trace_file) {
+        cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
+        cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
+      }
+#endif
       e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, tma_store, plan->num_sms, st);
+#ifdef TCBF_DEV
+      if (trace_file) {
+        std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
+        cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(a.trace);
+        if (FILE* f = fopen(trace_file, "wb")) {
+          fwrite(h.data(), 8, h.size(), f);
+          fclose(f);
+        }
+      }
+#endif
     } else if (plan->b1_kernel == TCBF_B1K_F4) {  // packed words by TMA: box {one 256-bit K block, 128 rows}
       CUtensorMap tw, tx;
       if (tma_store) {
@@ -511,9 +531,10 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_SMAJ) {
-    // weights as the stacked K-major B operand: box {64 K, 128 beams} per plane, 128-byte swizzle
+    // weights as the stacked K-major B operand: boxes {64 K, 64 beams} of a plane, 128-byte swizzle
+    // (a stage is four boxes, split among the CTAs of a multicast cluster)
     CUtensorMap tw;
-    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 64,
                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
     tcbf::GemmF16Args a;
@@ -534,8 +555,8 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
       cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
     }
 #endif
-    cudaError_t e = tcbf::launch_gemm_f16_smaj(tw, a, x_src, (int)layout, (int)plan->K, plan->smaj_epi_warps,
-                                               plan->f16_multicast != 0, plan->num_sms, st);
+    cudaError_t e = tcbf::launch_gemm_f16_smaj(tw, a, x_src, (int)layout, (int)plan->K, plan->smaj_cluster,
+                                               plan->num_sms, st);
 #ifdef TCBF_DEV
     if (trace_file) {
       std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);

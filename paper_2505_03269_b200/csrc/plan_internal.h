@@ -25,7 +25,7 @@ struct tcbf_plan_s {
   int f16_variant;    // tcbf::F16_V_*
   int f16_multicast;  // beam-major fused kernel: weight tiles multicast across CTA pairs
   int f16_fused_kind; // TCBF_FUSED_*: which fused fp32-data kernel tcbf_beamform_raw runs
-  int smaj_epi_warps; // sample-major fused kernel: epilogue warps (4 or 8)
+  int smaj_cluster;   // sample-major fused kernel: weight-multicast cluster size (1 or 2)
   int raw_mode;       // TCBF_RAW_*: what tcbf_beamform_raw runs
   int conv_splits_override;  // streaming-conversion K split (0 = by shape)
   int b1_kernel;      // TCBF_B1K_*: fp4 +-1 tensor cores (default), int8 AND form, legacy b1 mma.sync, popc

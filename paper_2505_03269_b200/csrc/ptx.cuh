@@ -132,19 +132,19 @@ __device__ __forceinline__ void cluster_sync() {
 }
 // TMA load multicast to both CTAs of a pair (same smem offset, each CTA's own barrier)
 __device__ __forceinline__ void tma_load_3d_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                               int32_t c1, int32_t c2) {
+                                               int32_t c1, int32_t c2, uint16_t mask = 3) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
       " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"((uint16_t)3)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
 // arrive on the barrier at this smem offset in BOTH CTAs of the pair when this thread's MMAs retire
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          smem_u32(bar))
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 

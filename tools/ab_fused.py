@@ -23,7 +23,7 @@ elif os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCB
     from paper_2505_03269_b200 import build as _b
     tcbf.library_path = _b.build_tcbf(dev=True)
 
-VARIANTS = [("smaj8", {}), ("smaj4", {"TCBF_SMAJ_EPI": "4"}), ("beam", {"TCBF_F16_FUSED": "beam"}),
+VARIANTS = [("smaj8", {}), ("smaj_mc0", {"TCBF_F16_MC": "0"}), ("beam", {"TCBF_F16_FUSED": "beam"}),
             ("beam_nomc", {"TCBF_F16_FUSED": "beam", "TCBF_F16_MC": "0"})]
 if os.environ.get("AB_VARIANTS"):   # e.g. "smaj8:,nostore:TCBF_DEBUG=1,nomma:TCBF_DEBUG=2"
     VARIANTS = []
@@ -47,7 +47,7 @@ def main():
     byts = B * (4 * M * K + 8 * K * N + 8 * M * N)
     reps = int(os.environ.get("AB_REPS", "2"))
     for name, env in VARIANTS * reps:    # interleaved repeats: the board heats up over a run
-        for k in ("TCBF_SMAJ_EPI", "TCBF_F16_FUSED", "TCBF_F16_MC", "TCBF_DEBUG"):
+        for k in ("TCBF_F16_FUSED", "TCBF_F16_MC", "TCBF_DEBUG"):
             os.environ.pop(k, None)
         os.environ.update(env)
         plan = tcbf.Plan(M, N, K, B, "f16")

@@ -30,9 +30,13 @@ KINDS = {
     5: ("tcgen05_mxf4", "tcgen05.mma kind::mxf4 block32 128x256x64, fp32 acc", 1.0),
     6: ("tcgen05_f16_ts_n64", "tcgen05.mma kind::f16 128x64x16, A from TMEM", 1.0),
     7: ("tcgen05_f16_ss_n128", "tcgen05.mma kind::f16 128x128x16, A and B from smem", 1.0),
+    8: ("tcgen05_mxf4_ts_n64", "tcgen05.mma kind::mxf4 block32 128x64x64, A from TMEM", 1.0),
+    9: ("tcgen05_mxf4_ss_n64", "tcgen05.mma kind::mxf4 block32 128x64x64, A and B from smem", 1.0),
+    10: ("tcgen05_mxf4_ts_n128", "tcgen05.mma kind::mxf4 block32 128x128x64, A from TMEM", 1.0),
 }
 # iterations per warp / issuing thread: each launch runs ~5-50 ms
-ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000, 6: 80000, 7: 80000}
+ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000, 6: 80000, 7: 80000, 8: 80000, 9: 80000,
+         10: 80000}
 
 
 def clocks():
@@ -48,7 +52,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--repeat", type=int, default=3)
+    ap.add_argument("--kinds", default=None, help="comma-separated kind numbers (default: all)")
     args = ap.parse_args()
+    kinds = [int(k) for k in args.kinds.split(",")] if args.kinds else list(KINDS)
     if not os.path.exists(LIB):
         sys.exit(f"{LIB} missing: run python -c 'import __graft_entry__ as g; g.build()'")
     lib = ctypes.CDLL(LIB)
@@ -56,7 +62,8 @@ def main():
                                   ctypes.POINTER(ctypes.c_double)]
     lib.tcbf_peak_run.restype = ctypes.c_int
     res = {}
-    for kind, (name, desc, useful) in KINDS.items():
+    for kind in kinds:
+        name, desc, useful = KINDS[kind]
         best = None
         for _ in range(args.repeat):
             s, o = ctypes.c_double(), ctypes.c_double()
