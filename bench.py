@@ -536,7 +536,8 @@ def measure(args, name, c, world, rank, local, dev, steps, warmup, e2e=False, en
         rec["clocks"] = sampler.summary()
 
     if energy:
-        rec["energy"] = energy_loop(step, stream, c, dev, world)
+        rec["energy"] = energy_loop(step, stream, c, dev, world,
+                                    shared_device=(world > 1 and args.dist_backend == "gloo"))
 
     if e2e:
         # through the public API with HOST buffers (pinned), copies inside the timed region
@@ -588,10 +589,11 @@ def measure(args, name, c, world, rank, local, dev, steps, warmup, e2e=False, en
     return rec
 
 
-def energy_loop(step, stream, c, dev, world, min_s=1.0):
+def energy_loop(step, stream, c, dev, world, min_s=1.0, shared_device=False):
     """NVML energy over a separate loop of >= `min_s` seconds of back-to-back steps (the counter's
     granularity makes short timed regions meaningless).  Board energy of this GPU; TeraOps/J of the
-    whole job = global ops / (joules summed over ranks)."""
+    whole job = global ops / (joules summed over ranks).  shared_device (the gloo test mode, every
+    rank on cuda:0): all ranks read the same board over the same loop, so the max is taken."""
     import torch
     from paper_2505_03269_b200.shard import sum_over_ranks
     s = ClockSampler(dev, sample=False)
@@ -614,7 +616,11 @@ def energy_loop(step, stream, c, dev, world, min_s=1.0):
     j = s.joules()
     if j is None or j <= 0:
         return {"unavailable": "NVML energy counter returned no delta"}
-    j_all = sum_over_ranks(j, dev)
+    if shared_device:
+        from paper_2505_03269_b200.shard import max_over_ranks
+        j_all = max_over_ranks(j, dev)
+    else:
+        j_all = sum_over_ranks(j, dev)
     watts = j / wall
     rec = {"joules_per_step": round(j_all / n, 6), "teraops_per_joule": round(useful_ops(c) * n / j_all / 1e12, 3),
            "loop_s": round(wall, 3), "steps": n, "avg_board_w": round(watts, 1),

@@ -172,6 +172,10 @@ void choose_kernels(tcbf_plan* p) {
     else if (strcmp(e, "f4") == 0 && tcbf::gemm_b1_f4_supported(p->kp)) p->b1_kernel = TCBF_B1K_F4;
   }
   p->b1_swap_beams = (p->b1_kernel == TCBF_B1K_F4 && !env_set("TCBF_NO_SWAP")) ? tcbf::gemm_b1_f4_swap_beams(p->M) : 0;
+  // experiment overrides: the swapped kernel (64-beam tiles) for any M; coalesced st.global
+  // epilogue instead of TMA stores
+  if (p->b1_kernel == TCBF_B1K_F4 && env_int("TCBF_B1_SWAP", 0) == 64) p->b1_swap_beams = 64;
+  p->b1_force_stg = env_int("TCBF_B1_STG", 0) != 0;
   // split-K of the int8 kernel: measured not to shorten the per-SM K chain, so only forced (tests)
   p->b1_splits = 1;
   p->b1_kb_per_split = (int)(p->kp / 4);
@@ -318,7 +322,7 @@ tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void*
     e = cudaMemsetAsync(out, 0, plan->out_bytes, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (split-K output)");
   }
-  const bool tma_store = (plan->N % 4) == 0;
+  const bool tma_store = (plan->N % 4) == 0 && !plan->b1_force_stg;
   tcbf_status s;
   if (plan->b1_kernel == TCBF_B1K_BMMA) {
     e = tcbf::launch_gemm_b1_mma(a, st);

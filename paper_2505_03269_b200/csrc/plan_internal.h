@@ -30,6 +30,7 @@ struct tcbf_plan_s {
   int conv_splits_override;  // streaming-conversion K split (0 = by shape)
   int b1_kernel;      // TCBF_B1K_*: fp4 +-1 tensor cores (default), int8 AND form, legacy b1 mma.sync, popc
   int b1_swap_beams;  // fp4 swapped small-M kernel: beams per tile (32 / 64), 0 = not used
+  int b1_force_stg;   // experiment: st.global epilogue instead of TMA stores
   int b1_splits, b1_kb_per_split;  // int8 split-K (forced only)
   int pack_wpt;       // 1-bit data pack words per thread (0 = by size)
   int debug;          // TCBF_DEV ablation bits (0 in product builds)

@@ -47,7 +47,7 @@ def main():
     byts = B * (4 * M * K + 8 * K * N + 8 * M * N)
     reps = int(os.environ.get("AB_REPS", "2"))
     for name, env in VARIANTS * reps:    # interleaved repeats: the board heats up over a run
-        for k in ("TCBF_F16_FUSED", "TCBF_F16_MC", "TCBF_DEBUG"):
+        for k in [k for k in os.environ if k.startswith("TCBF_")]:   # every override of the previous variant
             os.environ.pop(k, None)
         os.environ.update(env)
         plan = tcbf.Plan(M, N, K, B, "f16")

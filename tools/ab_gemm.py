@@ -35,7 +35,7 @@ def main():
     byts = B * ((M * K + K * N) / 4.0 + 8 * M * N) if prec == "b1" else B * (4 * M * K + 4 * K * N + 8 * M * N)
     ref = None
     for name, env in variants * int(os.environ.get("AB_REPS", "1")):
-        for k in ("TCBF_DEBUG", "TCBF_B1_KERNEL", "TCBF_NO_SWAP", "TCBF_B1_SPLITS", "TCBF_F16_VARIANT"):
+        for k in [k for k in os.environ if k.startswith("TCBF_")]:   # every override of the previous variant
             os.environ.pop(k, None)
         os.environ.update(env)
         plan = tcbf.Plan(M, N, K, B, prec)
