@@ -257,49 +257,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
 
   if (warp == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      // kind::mxf4 block32: A, B e2m1 (format 1), UE8M0 scales, fp32 D, K-major, M = 128, N = 256
-      constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) | (1u << 23) |
-                                 ((uint32_t)(BM >> 4) << 24);
-      const uint32_t sfa = tmem_base + C::SFC, sfb = tmem_base + C::SFC + C::SFB_OFF;
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-        mbar_wait(tempty_bar, (it & 1) ^ 1);
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers)
+    // kind::mxf4 block32: A, B e2m1 (format 1), UE8M0 scales, fp32 D, K-major, M = 128, N = 256
+    constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * BN) >> 3) << 17) | (1u << 23) |
+                               ((uint32_t)(BM >> 4) << 24);
+    const uint32_t sfa = tmem_base + C::SFC, sfb = tmem_base + C::SFC + C::SFB_OFF;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      mbar_wait(tempty_bar, (it & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base;  // [D_r | D_i]
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base;  // [D_r | D_i]
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          uint8_t* st = smem + stage * C::STAGE;
-          uint8_t* sAr = st;
-          uint8_t* sAi = st + TILE_BYTES;
-          uint8_t* sBn = st + C::BOFF;  // -B_i, B_r, B_i: consecutive 128-row tiles
-          uint8_t* sBr = sBn + TILE_BYTES;
-          const uint32_t ta = tmem_base + C::A_COL + 64 * stage;  // ATMEM: A_r columns, A_i at +32
+        const uint8_t* st = smem + stage * C::STAGE;
+        const uint8_t* sBn = st + C::BOFF;  // -B_i, B_r, B_i: consecutive 128-row tiles
+        // K advance per MMA: 64 nibbles = 32 bytes = +2 in the descriptor address field
+        const uint64_t ar0 = smem_desc_k128(st, 0), ai0 = smem_desc_k128(st + TILE_BYTES, 0);
+        const uint64_t b_ri0 = smem_desc_k128(sBn + TILE_BYTES, 0);  // [B_r; B_i]
+        const uint64_t b_nr0 = smem_desc_k128(sBn, 0);               // [-B_i; B_r]
+        const uint32_t ta = tmem_base + C::A_COL + 64 * stage;      // ATMEM: A_r columns, A_i at +32
+        if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements (32 bytes) per MMA
-            const uint32_t off = kk * 32;
-            const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
-            const uint64_t b_ri = smem_desc_k128(sBr, off);  // [B_r; B_i]
-            const uint64_t b_nr = smem_desc_k128(sBn, off);  // [-B_i; B_r]
+            const uint64_t b_ri = b_ri0 + (uint64_t)(2 * kk), b_nr = b_nr0 + (uint64_t)(2 * kk);
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             if (TCBF_ABLATE(p, 2)) continue;
             if constexpr (ATMEM) {  // K = 64 nibbles = 8 TMEM columns per MMA
               mma_mxf4_ts(d, ta + kk * 8, b_ri, IDESC, sfa, sfb, acc);
               mma_mxf4_ts(d, ta + 32 + kk * 8, b_nr, IDESC, sfa, sfb, 1u);
             } else {
-              mma_mxf4(d, ar, b_ri, IDESC, sfa, sfb, acc);  // [Re(a)Re(b) | Re(a)Im(b)]
-              mma_mxf4(d, ai, b_nr, IDESC, sfa, sfb, 1u);   // [-Im(a)Im(b) | Im(a)Re(b)]
+              mma_mxf4(d, ar0 + (uint64_t)(2 * kk), b_ri, IDESC, sfa, sfb, acc);  // [Re(a)Re(b) | Re(a)Im(b)]
+              mma_mxf4(d, ai0 + (uint64_t)(2 * kk), b_nr, IDESC, sfa, sfb, 1u);   // [-Im(a)Im(b) | Im(a)Re(b)]
             }
           }
           mma_commit(&empty_bar[stage]);
-          if (++stage == C::NST) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull_bar);
+        __syncwarp();
+        if (++stage == C::NST) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(tfull_bar);
+      __syncwarp();
     }
   } else if (warp <= EPI_WARPS) {
     // ------------------------------------------------------------ epilogue

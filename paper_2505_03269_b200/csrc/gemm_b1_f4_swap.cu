@@ -48,11 +48,13 @@ constexpr int PKB = 4;    // K blocks per packed TMA stage (128-byte rows of wor
 constexpr int EPI_WARPS = 4;
 constexpr int XEXP_WARPS = 4;
 constexpr int WEXP_WARPS = 4;
-constexpr int NST = 3;    // expanded stages (data in TMEM, weights in smem)
 constexpr uint32_t TMEM_COLS = 512;
 
 template <int TM>
 struct SwapCfg {
+  // expanded stages (data in TMEM, weights in smem): as many as TMEM holds beside the accumulators
+  // and the scale factors (the MMAs of a stage complete ~2.5 stages after their issue)
+  static constexpr int NST = TM == 32 ? 5 : 3;
   static constexpr int W_TILE = TM * 128;                 // one expanded weight tile
   static constexpr int STAGE_BYTES = 3 * W_TILE;           // -W_i, W_r, W_i
   static constexpr int P_PLANE_X = TN * PKB * KBW * 4;     // packed words: 128 rows x 128 B
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
                             int num_tiles) {
   using C = SwapCfg<TM>;
   constexpr int P_STAGES = C::P_STAGES;
+  constexpr int NST = C::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* packed = smem + C::P_OFFSET;
@@ -215,42 +218,45 @@ __global__ void __launch_bounds__(SwapCfg<TM>::NUM_THREADS, 1)
   tc_fence_after();
 
   if (warp == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      // kind::mxf4 block32: e2m1 A/B, UE8M0 scales, fp32 D, K-major, M = 128 samples, N = 2 TM
-      constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * TM) >> 3) << 17) | (1u << 23) |
-                                 ((uint32_t)(TN >> 4) << 24);
-      const uint32_t sfa = tmem_base + C::SF_COL, sfb = tmem_base + C::SF_COL + 32;
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-        const int abuf = it & 1;
-        mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers -- issuing from `lane == 0` cost an
+    // elect/broadcast loop per instruction, ~2.4x the small-N MMA's own time)
+    // kind::mxf4 block32: e2m1 A/B, UE8M0 scales, fp32 D, K-major, M = 128 samples, N = 2 TM
+    constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | ((uint32_t)((2 * TM) >> 3) << 17) | (1u << 23) |
+                               ((uint32_t)(TN >> 4) << 24);
+    const uint32_t sfa = tmem_base + C::SF_COL, sfb = tmem_base + C::SF_COL + 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int abuf = it & 1;
+      mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + abuf * 2 * TM;  // [D_r^T | D_i^T]
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
-        const uint32_t d = tmem_base + abuf * 2 * TM;  // [D_r^T | D_i^T]
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
-          tc_fence_after();
-          if (it == 0 && kb < 128) stamp(p.trace, kb);  // dev timeline: MMA got stage kb
-          uint8_t* sWn = smem + stage * C::STAGE_BYTES;  // -W_i, W_r, W_i: consecutive TM-row tiles
-          uint8_t* sWr = sWn + C::W_TILE;
-          const uint32_t xa = tmem_base + C::X_COL + 64 * stage;  // X_r columns, X_i at +32
+        if (it == 0 && kb < 128 && lane == 0) stamp(p.trace, kb);  // dev timeline: MMA got stage kb
+        const uint8_t* sWn = smem + stage * C::STAGE_BYTES;  // -W_i, W_r, W_i: consecutive TM-row tiles
+        const uint64_t w_nr = smem_desc_k128(sWn, 0);            // [-W_i; W_r]
+        const uint64_t w_ri = smem_desc_k128(sWn + C::W_TILE, 0);  // [W_r; W_i]
+        const uint32_t xa = tmem_base + C::X_COL + 64 * stage;  // X_r columns, X_i at +32
+        if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements = 32 bytes = 8 TMEM columns per MMA
-            const uint64_t w_ri = smem_desc_k128(sWr, kk * 32);  // [W_r; W_i]
-            const uint64_t w_nr = smem_desc_k128(sWn, kk * 32);  // [-W_i; W_r]
+          for (int kk = 0; kk < KBW / 2; ++kk) {  // K = 64 elements = 32 bytes (+2 in the descriptor) = 8 TMEM columns
             const uint32_t acc = (kb | kk) ? 1u : 0u;
             if (TCBF_ABLATE(p, 2)) continue;
-            mma_mxf4_ts(d, xa + kk * 8, w_ri, IDESC, sfa, sfb, acc);
-            mma_mxf4_ts(d, xa + 32 + kk * 8, w_nr, IDESC, sfa, sfb, 1u);
+            mma_mxf4_ts(d, xa + kk * 8, w_ri + (uint64_t)(2 * kk), IDESC, sfa, sfb, acc);
+            mma_mxf4_ts(d, xa + 32 + kk * 8, w_nr + (uint64_t)(2 * kk), IDESC, sfa, sfb, 1u);
           }
           mma_commit(&empty_bar[stage]);
-          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[abuf]);
-        if (it == 0) stamp(p.trace, 1000);
+        __syncwarp();
+        if (++stage == NST) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) mma_commit(&tfull[abuf]);
+      __syncwarp();
+      if (it == 0 && lane == 0) stamp(p.trace, 1000);
     }
   } else if (warp <= EPI_WARPS) {
     // ------------------------------------------------------------ epilogue (lane = sample)

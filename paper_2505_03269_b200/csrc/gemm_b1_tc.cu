@@ -132,8 +132,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers)
+    {
       // kind::i8, unsigned A and B, int32 D, K-major, M = 128, N = 2 BN: one MMA covers both
       // accumulators [D_r | D_i] (contiguous TMEM columns) against two stacked data tiles, so A
       // is read from smem once per pair of sub-products (the stage holds ~B_i, B_r, B_i in row
@@ -153,26 +154,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * STAGE_BYTES;
-          uint8_t* sAr = st;
-          uint8_t* sAi = st + TILE_BYTES;
-          uint8_t* sBc = st + 2 * TILE_BYTES;  // ~B_i, B_r, B_i: consecutive 128-row tiles
-          uint8_t* sBr = st + 3 * TILE_BYTES;
+          const uint8_t* st = smem + stage * STAGE_BYTES;
+          // K advance per MMA: 32 bytes (+2 in the descriptor address field)
+          const uint64_t ar0 = smem_desc_k128(st, 0), ai0 = smem_desc_k128(st + TILE_BYTES, 0);
+          const uint64_t b_cr0 = smem_desc_k128(st + 2 * TILE_BYTES, 0);  // [~B_i; B_r]
+          const uint64_t b_ri0 = smem_desc_k128(st + 3 * TILE_BYTES, 0);  // [B_r; B_i]
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // K = 32 bytes per MMA
-            const uint32_t off = kk * 32;
-            const uint64_t ar = smem_desc_k128(sAr, off), ai = smem_desc_k128(sAi, off);
-            const uint64_t b_ri = smem_desc_k128(sBr, off);  // [B_r; B_i]
-            const uint64_t b_cr = smem_desc_k128(sBc, off);  // [~B_i; B_r]
-            const uint32_t acc = ((kb - kb0) | kk) ? 1u : 0u;
-            if (TCBF_ABLATE(p, 2)) continue;
-            mma_i8_ss(d_re, ar, b_ri, IDESC, acc);  // [P(A_r & B_r) | P(A_r & B_i)]
-            mma_i8_ss(d_re, ai, b_cr, IDESC, 1u);   // [P(A_i & ~B_i) | P(A_i & B_r)]
+            for (int kk = 0; kk < 4; ++kk) {  // K = 32 bytes per MMA
+              const uint32_t acc = ((kb - kb0) | kk) ? 1u : 0u;
+              if (TCBF_ABLATE(p, 2)) continue;
+              mma_i8_ss(d_re, ar0 + (uint64_t)(2 * kk), b_ri0 + (uint64_t)(2 * kk), IDESC, acc);  // [P(A_r & B_r) | P(A_r & B_i)]
+              mma_i8_ss(d_re, ai0 + (uint64_t)(2 * kk), b_cr0 + (uint64_t)(2 * kk), IDESC, 1u);   // [P(A_i & ~B_i) | P(A_i & B_r)]
+            }
+            mma_commit(&empty_bar[stage]);
           }
-          mma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull_bar[abuf]);
+        if (elect_one()) mma_commit(&tfull_bar[abuf]);
+        __syncwarp();
       }
     }
   } else if (warp <= 4) {

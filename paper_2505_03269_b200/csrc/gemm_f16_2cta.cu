@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader CTA only)
-    if (leader && lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA only;
+    // converged warp, one elected lane issues: descriptors stay in uniform registers)
+    if (leader) {
       constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) | ((256u >> 4) << 24);
       constexpr uint32_t IDESC_NEG = IDESC | (1u << 13);
       int stage = 0;
@@ -191,26 +192,31 @@ __global__ void __launch_bounds__(Cfg2<BN, STAGES>::NUM_THREADS, 1)
         for (int kb = 0; kb < args.num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
-          uint8_t* sAr = st;
-          uint8_t* sAi = st + Cfg::A_BYTES;
-          uint8_t* sBr = st + 2 * Cfg::A_BYTES;
-          uint8_t* sBi = sBr + Cfg::B_BYTES;
+          const uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+          // K advance per MMA: 16 K = 32 bytes of the K-major A (+2 in the address field), 16
+          // k-rows = 2048 bytes of the MN-major B (+128)
+          const uint64_t ar0 = desc_a128(st, 0), ai0 = desc_a128(st + Cfg::A_BYTES, 0);
+          const uint64_t br0 = desc_b_mn(st + 2 * Cfg::A_BYTES, 0);
+          const uint64_t bi0 = desc_b_mn(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, 0);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ar = desc_a128(sAr, kk * 32), ai = desc_a128(sAi, kk * 32);
-            const uint64_t br = desc_b_mn(sBr, kk * 16), bi = desc_b_mn(sBi, kk * 16);
-            const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (TCBF_ABLATE(args, 2)) continue;
-            mma_f16_2sm(d_re, ar, br, IDESC, acc);
-            mma_f16_2sm(d_re, ai, bi, IDESC_NEG, 1u);
-            mma_f16_2sm(d_im, ar, bi, IDESC, acc);
-            mma_f16_2sm(d_im, ai, br, IDESC, 1u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ar = ar0 + (uint64_t)(2 * kk), ai = ai0 + (uint64_t)(2 * kk);
+              const uint64_t br = br0 + (uint64_t)(128 * kk), bi = bi0 + (uint64_t)(128 * kk);
+              const uint32_t acc = (kb | kk) ? 1u : 0u;
+              if (TCBF_ABLATE(args, 2)) continue;
+              mma_f16_2sm(d_re, ar, br, IDESC, acc);
+              mma_f16_2sm(d_re, ai, bi, IDESC_NEG, 1u);
+              mma_f16_2sm(d_im, ar, bi, IDESC, acc);
+              mma_f16_2sm(d_im, ai, br, IDESC, 1u);
+            }
+            mma_commit_2sm_mc(&empty_bar[stage]);  // frees the stage in both CTAs
           }
-          mma_commit_2sm_mc(&empty_bar[stage]);  // frees the stage in both CTAs
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit_2sm_mc(&tfull_bar[abuf]);  // accumulators ready in both CTAs
+        if (elect_one()) mma_commit_2sm_mc(&tfull_bar[abuf]);  // accumulators ready in both CTAs
+        __syncwarp();
       }
     }
   } else {

@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers)
+    {
       constexpr uint32_t IDESC = (1u << 4) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       constexpr uint32_t IDESC_NEG = IDESC | (1u << 13);
       int stage = 0;
@@ -191,25 +192,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * STAGE_BYTES;
-          uint8_t* sAr = st;
-          uint8_t* sAi = st + A_BYTES;
-          uint8_t* sBr = st + 2 * A_BYTES;
-          uint8_t* sBi = sBr + B_BYTES;
+          const uint8_t* st = smem + stage * STAGE_BYTES;
+          // K advance per MMA: 32 bytes of the K-major A (+2), 16 k-rows of the MN-major B (+128)
+          const uint64_t ar0 = desc_a64(st, 0), ai0 = desc_a64(st + A_BYTES, 0);
+          const uint64_t br0 = desc_b_mn(st + 2 * A_BYTES, 0), bi0 = desc_b_mn(st + 2 * A_BYTES + B_BYTES, 0);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ar = desc_a64(sAr, kk * 32), ai = desc_a64(sAi, kk * 32);
-            const uint64_t br = desc_b_mn(sBr, kk * 16), bi = desc_b_mn(sBi, kk * 16);
-            const uint32_t acc = (kb != w.kb0 || kk) ? 1u : 0u;
-            mma_f16_ss(d_re, ar, br, IDESC, acc);
-            mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);
-            mma_f16_ss(d_im, ar, bi, IDESC, acc);
-            mma_f16_ss(d_im, ai, br, IDESC, 1u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ar = ar0 + (uint64_t)(2 * kk), ai = ai0 + (uint64_t)(2 * kk);
+              const uint64_t br = br0 + (uint64_t)(128 * kk), bi = bi0 + (uint64_t)(128 * kk);
+              const uint32_t acc = (kb != w.kb0 || kk) ? 1u : 0u;
+              mma_f16_ss(d_re, ar, br, IDESC, acc);
+              mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);
+              mma_f16_ss(d_im, ar, bi, IDESC, acc);
+              mma_f16_ss(d_im, ai, br, IDESC, 1u);
+            }
+            mma_commit(&empty_bar[stage]);
           }
-          mma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[abuf]);
+        if (elect_one()) mma_commit(&tfull[abuf]);
+        __syncwarp();
       }
     }
   } else if (warp < 2 + EPI_WARPS) {

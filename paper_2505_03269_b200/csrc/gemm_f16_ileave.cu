@@ -151,8 +151,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers)
+    {
       // kind::f16: fp16 A (MN-major, bit 15) and B (K-major), fp32 D, M = 128, N = 256
       constexpr uint32_t IDESC = (1u << 4) | (1u << 15) | ((uint32_t)((2 * BB) >> 3) << 17) |
                                  ((uint32_t)(BSR >> 4) << 24);
@@ -167,19 +168,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < args.num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * STAGE_BYTES;
+          const uint8_t* st = smem + stage * STAGE_BYTES;
+          // K advance per MMA: 16 k-rows of the MN-major data (+128), 32 bytes of the weights (+2)
+          const uint64_t x0 = desc_x(st + 2 * W_TILE, 0), w0 = desc_w(st, 0);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t x = desc_x(st + 2 * W_TILE, kk * 16);
-            const uint64_t w = desc_w(st, kk * 32);
-            if (TCBF_ABLATE(args, 2)) continue;
-            mma_f16_ss(d, x, w, IDESC, (kb | kk) ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              if (TCBF_ABLATE(args, 2)) continue;
+              mma_f16_ss(d, x0 + (uint64_t)(128 * kk), w0 + (uint64_t)(2 * kk), IDESC, (kb | kk) ? 1u : 0u);
+            }
+            if (MC) mma_commit_mc(&empty_bar[stage]);  // the stage is free in both CTAs
+            else mma_commit(&empty_bar[stage]);
           }
-          if (MC) mma_commit_mc(&empty_bar[stage]);  // the stage is free in both CTAs
-          else mma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[abuf]);
+        if (elect_one()) mma_commit(&tfull[abuf]);
+        __syncwarp();
       }
     }
   } else {

@@ -149,8 +149,9 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers)
+    {
       constexpr uint32_t IDESC = idesc_f16_mn(BM, BN, false);
       constexpr uint32_t IDESC_NEG = idesc_f16_mn(BM, BN, true);
       int stage = 0;
@@ -166,26 +167,30 @@ __global__ void __launch_bounds__(F16Cfg<BN, BK, STAGES, EPI_WARPS, EPI>::NUM_TH
         for (int kb = 0; kb < args.num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
-          uint8_t* sAr = st;
-          uint8_t* sAi = st + Cfg::A_BYTES;
-          uint8_t* sBr = st + 2 * Cfg::A_BYTES;
-          uint8_t* sBi = sBr + Cfg::B_BYTES;
+          const uint8_t* st = smem + stage * Cfg::STAGE_BYTES;
+          // K advance per MMA: 32 bytes of the K-major A (+2), 16 k-rows of the MN-major B (+128)
+          const uint64_t ar0 = desc_a<BK>(st, 0), ai0 = desc_a<BK>(st + Cfg::A_BYTES, 0);
+          const uint64_t br0 = desc_b_mn<BK>(st + 2 * Cfg::A_BYTES, 0);
+          const uint64_t bi0 = desc_b_mn<BK>(st + 2 * Cfg::A_BYTES + Cfg::B_BYTES, 0);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ar = desc_a<BK>(sAr, kk * 32), ai = desc_a<BK>(sAi, kk * 32);
-            const uint64_t br = desc_b_mn<BK>(sBr, kk * 16), bi = desc_b_mn<BK>(sBi, kk * 16);
-            const uint32_t acc = (kb | kk) ? 1u : 0u;
-            if (TCBF_ABLATE(args, 2)) continue;
-            mma_f16_ss(d_re, ar, br, IDESC, acc);     // Re += Re(a) Re(b)
-            mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);  // Re += -Im(a) Im(b)
-            mma_f16_ss(d_im, ar, bi, IDESC, acc);     // Im += Re(a) Im(b)
-            mma_f16_ss(d_im, ai, br, IDESC, 1u);      // Im += Im(a) Re(b)
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ar = ar0 + (uint64_t)(2 * kk), ai = ai0 + (uint64_t)(2 * kk);
+              const uint64_t br = br0 + (uint64_t)(128 * kk), bi = bi0 + (uint64_t)(128 * kk);
+              const uint32_t acc = (kb | kk) ? 1u : 0u;
+              if (TCBF_ABLATE(args, 2)) continue;
+              mma_f16_ss(d_re, ar, br, IDESC, acc);     // Re += Re(a) Re(b)
+              mma_f16_ss(d_re, ai, bi, IDESC_NEG, 1u);  // Re += -Im(a) Im(b)
+              mma_f16_ss(d_im, ar, bi, IDESC, acc);     // Im += Re(a) Im(b)
+              mma_f16_ss(d_im, ai, br, IDESC, 1u);      // Im += Im(a) Re(b)
+            }
+            mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
           }
-          mma_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull_bar[abuf]);  // accumulator ready for the epilogue
+        if (elect_one()) mma_commit(&tfull_bar[abuf]);  // accumulator ready for the epilogue
+        __syncwarp();
       }
     }
   } else {

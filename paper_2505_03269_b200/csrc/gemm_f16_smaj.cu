@@ -179,65 +179,71 @@ __global__ void __launch_bounds__(SCfg<EPI_WARPS>::NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t I256 = idesc_smaj(2 * BB, false);
-      constexpr uint32_t I128 = idesc_smaj(BB, false);
-      constexpr uint32_t I128_NEG = idesc_smaj(BB, true);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0, ui = 0;
-      for (int u = u_first; u < num_units; u += u_step, ++ui) {
-        const uint32_t xphase = ui & 1;
-        for (int mt = 0; mt < tiles_m; ++mt, ++it) {
-          const int abuf = it & 1;
-          const unsigned long long tw0 = args.trace ? gtimer() : 0;  // dev timeline (tools/trace_smaj.py)
-          mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
-          tc_fence_after();
-          unsigned long long wwait = 0, xwait = 0;
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues: descriptors stay in uniform registers; issuing from `lane == 0` made the
+    // compiler wrap every MMA in an elect/broadcast loop)
+    constexpr uint32_t I256 = idesc_smaj(2 * BB, false);
+    constexpr uint32_t I128 = idesc_smaj(BB, false);
+    constexpr uint32_t I128_NEG = idesc_smaj(BB, true);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, ui = 0;
+    for (int u = u_first; u < num_units; u += u_step, ++ui) {
+      const uint32_t xphase = ui & 1;
+      for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+        const int abuf = it & 1;
+        const unsigned long long tw0 = args.trace ? gtimer() : 0;  // dev timeline (tools/trace_smaj.py)
+        mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        unsigned long long wwait = 0, xwait = 0;
+        if (args.trace && lane == 0) {
+          stamp(args.trace, 4 * it);
+          stamp_val(args.trace, 512 + 4 * it + 3, gtimer() - tw0);
+        }
+        const uint32_t d_re = tmem_base + abuf * 2 * BB;  // [Re | Im]: 256 columns
+        const uint32_t d_im = d_re + BB;
+        for (int kb = 0; kb < num_kb; ++kb) {
           if (args.trace) {
-            stamp(args.trace, 4 * it);
-            stamp_val(args.trace, 512 + 4 * it + 3, gtimer() - tw0);
-          }
-          const uint32_t d_re = tmem_base + abuf * 2 * BB;  // [Re | Im]: 256 columns
-          const uint32_t d_im = d_re + BB;
-          for (int kb = 0; kb < num_kb; ++kb) {
-            if (args.trace) {
-              const unsigned long long a0 = gtimer();
-              if (mt == 0) mbar_wait(&xfull[kb], xphase);
-              const unsigned long long a1 = gtimer();
-              mbar_wait(&wfull[stage], phase);
-              xwait += a1 - a0;
-              wwait += gtimer() - a1;
-            }
-            if (mt == 0) mbar_wait(&xfull[kb], xphase);  // resident data block converted
+            const unsigned long long a0 = gtimer();
+            if (mt == 0) mbar_wait(&xfull[kb], xphase);
+            const unsigned long long a1 = gtimer();
             mbar_wait(&wfull[stage], phase);
-            tc_fence_after();
-            uint8_t* st = sW + stage * W_STAGE;
+            xwait += a1 - a0;
+            wwait += gtimer() - a1;
+          }
+          if (mt == 0) mbar_wait(&xfull[kb], xphase);  // resident data block converted
+          mbar_wait(&wfull[stage], phase);
+          tc_fence_after();
+          const uint8_t* st = sW + stage * W_STAGE;
+          const uint64_t xr0 = desc_x(sX, kb * BK), xi0 = desc_x(sX + X_PLANE, kb * BK);
+          const uint64_t wri0 = desc_w(st, 0);           // [W_r ; W_i], N = 256 (W_r alone: N = 128)
+          const uint64_t wi0 = desc_w(st + W_TILE, 0);   // W_i, N = 128
+          if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint32_t krow = kb * BK + kk * 16;
-              const uint64_t xr = desc_x(sX, krow), xi = desc_x(sX + X_PLANE, krow);
-              const uint64_t w_ri = desc_w(st, kk * 32);            // [W_r ; W_i], N = 256
-              const uint64_t w_i = desc_w(st + W_TILE, kk * 32);    // W_i, N = 128
-              const uint64_t w_r = w_ri;                            // W_r, N = 128
+              // K advance: 16 k-rows of the MN-major data = 2048 B (+128 in the address field),
+              // 16 K of the K-major weights = 32 B (+2)
+              const uint64_t xr = xr0 + (uint64_t)(128 * kk), xi = xi0 + (uint64_t)(128 * kk);
+              const uint64_t w_ri = wri0 + (uint64_t)(2 * kk), w_i = wi0 + (uint64_t)(2 * kk);
               const uint32_t acc = (kb | kk) ? 1u : 0u;
               if (TCBF_ABLATE(args, 2)) continue;
               mma_f16_ss(d_re, xr, w_ri, I256, acc);      // [Re | Im] += X_r [W_r ; W_i]^T
               mma_f16_ss(d_re, xi, w_i, I128_NEG, 1u);    // Re += -X_i W_i^T
-              mma_f16_ss(d_im, xi, w_r, I128, 1u);        // Im += X_i W_r^T
+              mma_f16_ss(d_im, xi, w_ri, I128, 1u);       // Im += X_i W_r^T
             }
             if (MC) mma_commit_mc(&wempty[stage], CL_MASK);  // the stage is free in every CTA of the cluster
             else mma_commit(&wempty[stage]);
             if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data block
-            if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
-          mma_commit(&tfull[abuf]);
-          if (args.trace) {
-            stamp(args.trace, 4 * it + 1);
-            stamp_val(args.trace, 512 + 4 * it, wwait);
-            stamp_val(args.trace, 512 + 4 * it + 1, xwait);
-          }
+          __syncwarp();
+          if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit(&tfull[abuf]);
+        __syncwarp();
+        if (args.trace && lane == 0) {
+          stamp(args.trace, 4 * it + 1);
+          stamp_val(args.trace, 512 + 4 * it, wwait);
+          stamp_val(args.trace, 512 + 4 * it + 1, xwait);
         }
       }
     }

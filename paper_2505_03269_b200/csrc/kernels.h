@@ -55,6 +55,13 @@ cudaError_t launch_gemm_f16_conv(const CUtensorMap& tmA, const CUtensorMap& tmX,
                                  const GemmF16Args& args, int layout, int num_sms, cudaStream_t stream);
 bool gemm_f16_smaj_supported(int64_t K16);
 // sample-major fused kernel (gemm_f16_smaj.cu): tiles_m = beam tiles, tiles_n = 128-sample tiles
+// resident-data interleaved fp16 kernel (gemm_f16_ileave_res.cu): tiles_m = 64-beam tiles,
+// tiles_n = 128-sample units, num_kb = K16 / 64 (K16 <= 256)
+bool gemm_f16_ileave_res_supported(int64_t K16);
+int gemm_f16_ileave_res_beams();
+int gemm_f16_ileave_res_samples();
+cudaError_t launch_gemm_f16_ileave_res(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
+                                       int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
                                  int K, int cluster, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,

@@ -201,6 +201,7 @@ void choose_kernels(tcbf_plan* p) {
     if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
   // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
   p->smaj_cluster = p->f16_multicast ? 2 : 1;
+  p->f16i_resident = tcbf::gemm_f16_ileave_res_supported(p->kp) && !env_set("TCBF_F16I_STREAM");
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
     const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ ? tcbf::gemm_f16_smaj_supported(p->kp)
                                                               : tcbf::gemm_f16_fused_supported(p->kp, p->N);
@@ -478,7 +479,8 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
-      return plan->prec == TCBF_PREC_F16 ? "f16_tcgen05_interleaved_smaj_64x128" : "none";
+      return plan->prec != TCBF_PREC_F16 ? "none"
+             : plan->f16i_resident ? "f16_tcgen05_interleaved_resident_128x64" : "f16_tcgen05_interleaved_smaj_64x128";
   }
   return "none";
 }
@@ -694,6 +696,34 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (plan->f16i_resident) {
+    // data resident per 128-sample unit, 64-beam tiles: weights box {64 K, 64 beams}; interleaved
+    // data as a real [B][K][2N] fp16 matrix, boxes {64 columns, 64 k-rows} (128-byte swizzle)
+    CUtensorMap tw, tx;
+    const int bb = tcbf::gemm_f16_ileave_res_beams(), bs = tcbf::gemm_f16_ileave_res_samples();
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, bb,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, x_f16, 2 * plan->N, plan->K, plan->B, 64, 64,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    a.multicast = plan->f16_multicast;
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + bb - 1) / bb);
+    a.tiles_n = (int)((plan->N + bs - 1) / bs);
+    a.num_kb = (int)(plan->kp / 64);
+    const int64_t nu = (int64_t)a.tiles_n * plan->B;
+    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+    a.num_tiles = (int)(nu * a.tiles_m);
+    a.out = static_cast<float*>(out);
+    a.debug = plan->debug;
+    cudaError_t e = tcbf::launch_gemm_f16_ileave_res(tw, tx, a, plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "interleaved-fp16 (resident) beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
   const int bk = tcbf::gemm_f16_ileave_block_k(), bnc = tcbf::gemm_f16_ileave_block_n();
   CUtensorMap ta, tx, tc;
   s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, bk, 128,
