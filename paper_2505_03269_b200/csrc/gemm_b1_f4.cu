@@ -77,10 +77,14 @@ constexpr uint32_t SF_COL = 256;  // scale factors: columns 256..511
 // registers) and the MMAs read A from TMEM; only the three data tiles stay in shared memory
 // (~30% less smem traffic per K block).  TMEM: [D_r | D_i] 0..255, A stages 256 + 64 s, scale
 // factors in the remaining columns.
+// Short K (register look-ahead words, the store-bound radio shape): the epilogue stages a warp's
+// WHOLE 32 x 128 output block (four 32 x 32 boxes, 16 KB) before one wait per tile, so the single
+// TMEM accumulator is released as soon as it is read, not after each box's TMA store has drained;
+// the 128 KB of staging this needs leaves room for two expanded stages (enough for K <= 1024).
 template <bool TMA_WORDS, bool ATMEM = false>
 struct Cfg {
   static constexpr int STAGE = ATMEM ? 3 * TILE_BYTES : STAGE_BYTES;  // smem bytes per stage
-  static constexpr int NST = ATMEM ? ATMEM_STAGES : STAGES;          // expanded-operand stages
+  static constexpr int NST = ATMEM ? (TMA_WORDS ? ATMEM_STAGES : 2) : STAGES;  // expanded-operand stages
   static constexpr int BOFF = ATMEM ? 0 : 2 * TILE_BYTES;             // -B_i, B_r, B_i tiles
   static constexpr uint32_t A_COL = 256;
   static constexpr uint32_t SFC = ATMEM ? A_COL + 64 * NST : SF_COL;
@@ -88,7 +92,8 @@ struct Cfg {
   static constexpr int P_STAGES = TMA_WORDS ? 2 : 0;
   static constexpr int BOX_COLS = TMA_WORDS ? 16 : 32;
   static constexpr int EPI_BOX = 32 * BOX_COLS * 4;
-  static constexpr int EPI_BYTES = EPI_WARPS * 2 * EPI_BOX;
+  static constexpr int EPI_BOXES = TMA_WORDS ? 2 : BN / BOX_COLS;  // per warp: double buffer / whole row
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_BOXES * EPI_BOX;
   static constexpr int P_OFFSET = NST * STAGE;
   static constexpr int EPI_OFFSET = P_OFFSET + P_STAGES * P_STAGE_BYTES;
   static constexpr int BAR_OFFSET = EPI_OFFSET + EPI_BYTES;
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;            // TMEM lane quarter this warp may access
     const int part = (warp - 1) >> 2;  // 0: Re (columns 0..127), 1: Im (128..255)
     constexpr int CHUNKS = BN / 32;
-    uint8_t* bufs = epi_base + (warp - 1) * 2 * EPI_BOX;
+    uint8_t* bufs = epi_base + (warp - 1) * C::EPI_BOXES * EPI_BOX;
     int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
@@ -317,6 +322,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int n0 = nt * BN;
       mbar_wait(tfull_bar, it & 1);
       tc_fence_after();
+      constexpr bool WHOLE = TMA_STORE && !TMA_WORDS;  // stage the whole row block, one wait per tile
+      if constexpr (WHOLE) {
+        if (lane == 0) bulk_wait_group_read<0>();  // the previous tile's boxes have been read out
+        __syncwarp();
+      }
       // ablation (TCBF_DEBUG bit 3; timing only, wrong values): release TMEM before reading it.
       // Measured upper bound of any early-release epilogue: +3-5% (square 8192^3 0.82 -> 0.79 ms)
       if ((TCBF_ABLATE(p, 8)) && lane == 0) mbar_arrive(tempty_bar);
@@ -342,7 +352,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < CW; ++j) vv[j] = (uint32_t)(__float2int_rn(__uint_as_float(vv[j])) - corr);
         if (TCBF_ABLATE(p, 1)) continue;
-        if constexpr (TMA_STORE) {  // 32-row boxes of BOX_COLS columns, double-buffered per warp
+        if constexpr (WHOLE) {  // chunk c -> box c * CW / BOX_COLS of this warp's row block
+          const int off = (c * CW) % BOX_COLS;
+          uint8_t* buf = bufs + ((c * CW) / BOX_COLS) * EPI_BOX;
+#pragma unroll
+          for (int j = 0; j < CW / 4; ++j) {  // 16-byte chunks, 128-byte swizzle
+            const int jj = off / 4 + j;
+            *reinterpret_cast<uint4*>(buf + lane * (BOX_COLS * 4) + ((jj ^ (lane & 7)) * 16)) =
+                make_uint4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+          }
+          if (c == NCH - 1) {  // all boxes staged: one TMA store each
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+              for (int x = 0; x < C::EPI_BOXES; ++x) tma_store_3d(&tmC, bufs + x * EPI_BOX, n0 + x * BOX_COLS, m0 + q * 32, 2 * b + part);
+              bulk_commit_group();
+            }
+          }
+        } else if constexpr (TMA_STORE) {  // 32-row boxes of BOX_COLS columns, double-buffered per warp
           const int off = (c * CW) % BOX_COLS;  // column of this chunk inside its box
           uint8_t* buf = bufs + sbuf * EPI_BOX;
           if (off == 0) {
