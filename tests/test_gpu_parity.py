@@ -335,6 +335,29 @@ def test_f16i_integer_inputs_exact(tcbf):
     assert np.array_equal(y.cpu().numpy().astype(np.float64), oracle.cgemm_f16(w, x, 0, M, N, K, B))
 
 
+@pytest.mark.parametrize("shape", [(256, 512, 200, 3), (130, 384, 256, 1), (70, 1000, 64, 2)])
+def test_f16i_resident_equals_streaming(tcbf, shape, monkeypatch):
+    """The resident-data NEXT-1 kernel (K16 <= 256: data loaded once per 128-sample unit, 64-beam
+    tiles, two N = 128 MMAs per K step) against the streaming one (TCBF_F16I_STREAM: data re-read
+    per beam tile, one N = 256 MMA): the same fp16 products accumulated in the same K order, so the
+    results agree to the last fp32 bit or within one rounding of the final Re/Im combination."""
+    M, N, K, B = shape
+    w = synth.generate("phase", 31, 0, B, M, K)
+    x = synth.to_interleaved(synth.generate("adc", 31, 1, B, K, N)).astype(np.float16)
+    xd = torch.from_numpy(x).cuda()
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    assert "resident" in plan.kernel("f16i")
+    wp = plan.pack(tcbf.WEIGHTS, _dev(synth.to_interleaved(w)))
+    y_res = plan.beamform_f16i(wp, xd)
+    monkeypatch.setenv("TCBF_F16I_STREAM", "1")
+    ps = tcbf.Plan(M, N, K, B, "f16")
+    assert "resident" not in ps.kernel("f16i")
+    y_str = ps.beamform_f16i(wp, xd)
+    torch.cuda.synchronize()
+    scale = y_str.abs().max().item()
+    assert (y_res - y_str).abs().max().item() <= 1e-6 * scale
+
+
 def test_f16i_errors(tcbf):
     plan = tcbf.Plan(8, 6, 8, 1, "f16")   # N % 4 != 0
     wp = plan.alloc_packed(tcbf.WEIGHTS)

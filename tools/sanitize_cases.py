@@ -43,8 +43,7 @@ def _f16_ok(y, ref):
 
 
 def run_case(name, prec, M, N, K, B, path="packed", env=None):
-    for k in ("TCBF_B1_KERNEL", "TCBF_NO_SWAP", "TCBF_F16_VARIANT", "TCBF_B1_SPLITS", "TCBF_NO_FUSED",
-              "TCBF_FORCE_STREAM_CONV", "TCBF_F16_MC"):
+    for k in [k for k in os.environ if k.startswith("TCBF_")]:   # the previous case's overrides
         os.environ.pop(k, None)
     os.environ.update(env or {})
     w, x = _srcs(M, N, K, B, 17 + M + N + K)
@@ -84,12 +83,16 @@ CASES = {
         ("f16_fused_raw_multicast", "f16", 200, 256, 100, 3, "raw", None),
         ("f16_stream_conv", "f16", 32, 260, 700, 1, "raw", {"TCBF_FORCE_STREAM_CONV": "1"}),
         ("f16_stream_conv_split", "f16", 40, 128, 3000, 1, "raw", {"TCBF_FORCE_STREAM_CONV": "1"}),
-        ("f16_interleaved", "f16", 200, 300, 100, 2, "f16i", None),
+        ("f16_interleaved_resident", "f16", 200, 300, 100, 2, "f16i", None),
+        ("f16_interleaved_resident_mc", "f16", 130, 256, 200, 3, "f16i", None),
+        ("f16_interleaved_streaming", "f16", 200, 300, 100, 2, "f16i", {"TCBF_F16I_STREAM": "1"}),
+        ("f16_interleaved_long_k", "f16", 100, 132, 333, 1, "f16i", None),
     ],
     "b1": [
         ("b1_f4_tiny", "b1", 8, 64, 32, 2, "packed", {"TCBF_NO_SWAP": "1"}),
         ("b1_f4_ragged", "b1", 130, 200, 1000, 2, "packed", None),
         ("b1_f4_masked", "b1", 100, 129, 31, 2, "packed", None),
+        ("b1_f4_short_k_rows", "b1", 200, 300, 500, 3, "packed", None),
         ("b1_f4_long_k_tma", "b1", 130, 96, 5000, 1, "packed", None),
         ("b1_f4_swap32", "b1", 17, 260, 700, 2, "packed", None),
         ("b1_f4_swap64", "b1", 48, 77, 600, 2, "packed", None),
