@@ -454,8 +454,9 @@ int gemm_b1_f4_swap_box_words() { return PKB * KBW; }
 // tensor maps: packed words [2B][rows][Kw] u32, box {32 words, 128 samples} (data) and
 // {32 words, TM beams} (weights), 128-byte swizzle, zero fill past Kw
 cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
-                                   const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream) {
-  if (gemm_b1_f4_swap_beams(args.M) == 32)
+                                   const GemmB1Args& args, int beams, bool tma_store, int num_sms, cudaStream_t stream) {
+  // beams per tile as the plan chose it (the weight tensor map's box was built for it)
+  if (beams == 32)
     return tma_store ? launch_swap<32, true>(tmW, tmX, tmC, args, num_sms, stream)
                      : launch_swap<32, false>(tmW, tmX, tmC, args, num_sms, stream);
   return tma_store ? launch_swap<64, true>(tmW, tmX, tmC, args, num_sms, stream)

@@ -88,7 +88,7 @@ int gemm_b1_f4_store_box_cols(int64_t Kw);
 int gemm_b1_f4_swap_beams(int64_t M);  // beams per tile of the swapped small-M kernel (0: not used)
 int gemm_b1_f4_swap_box_words();        // packed words per TMA box row of the swapped kernel
 cudaError_t launch_gemm_b1_f4_swap(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
-                                   const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
+                                   const GemmB1Args& args, int beams, bool tma_store, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_b1_f4(const CUtensorMap& tmW, const CUtensorMap& tmX, const CUtensorMap& tmC,
                               const GemmB1Args& args, bool tma_store, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_b1_tc(const CUtensorMap& tmC, const GemmB1Args& args, bool tma_store, int num_sms,

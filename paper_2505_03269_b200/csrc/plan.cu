@@ -355,7 +355,7 @@ tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void*
         cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
       }
 #endif
-      e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, tma_store, plan->num_sms, st);
+      e = tcbf::launch_gemm_b1_f4_swap(tw, tx, tc, a, plan->b1_swap_beams, tma_store, plan->num_sms, st);
 #ifdef TCBF_DEV
       if (trace_file) {
         std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);

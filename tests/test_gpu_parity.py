@@ -583,6 +583,19 @@ def test_b1_small_m_swapped_kernel_bit_exact(tcbf, shape):
     assert np.array_equal(y, oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B))
 
 
+@pytest.mark.parametrize("shape", [(32, 300, 700, 2), (200, 260, 500, 1)])
+def test_b1_forced_swap64_bit_exact(tcbf, shape, monkeypatch):
+    """TCBF_B1_SWAP=64 (experiment override): the swapped kernel with 64-beam tiles for any M,
+    including M <= 32 where the default picks 32-beam tiles (the tile width follows the plan)."""
+    monkeypatch.setenv("TCBF_B1_SWAP", "64")
+    M, N, K, B = shape
+    w = synth.generate("adc", 43, 0, B, M, K)
+    x = synth.generate("adc", 43, 1, B, K, N)
+    plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    assert "swap_128x64" in plan.variant
+    assert np.array_equal(y, oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B))
+
+
 def test_full_size_m32_b1_16384(tcbf):
     """BASELINE configs[4] small-beam 1-bit point M=32, N=K=16384 at full size, whole output."""
     M = 32
