@@ -13,7 +13,9 @@ import torch  # noqa: E402
 import paper_2505_03269_b200 as tcbf  # noqa: E402
 import synth  # noqa: E402
 
-if os.environ.get("AB_DEV_LIB"):
+if os.environ.get("AB_LIB"):       # a specific build (e.g. the previous commit's, for an A/B)
+    tcbf.library_path = os.environ["AB_LIB"]
+elif os.environ.get("AB_DEV_LIB"):
     from paper_2505_03269_b200 import build as _b
     tcbf.library_path = _b.build_tcbf(dev=True)
 

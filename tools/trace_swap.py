@@ -1,6 +1,7 @@
 """Dev tool: timeline of the swapped small-M 1-bit kernel's first tile (TCBF_TRACE, dev build):
-per K block when the packed words were requested / landed, when the data expander got the
-stage / handed it over, when the weight expander handed it over, when the MMA issuer got it."""
+per K block when the packed words were requested, when the data expander got the stage / handed
+its block over, when the weight expanders handed the stage (two K blocks) over, when the MMA
+issuer got the stage."""
 import os
 import sys
 
@@ -30,8 +31,8 @@ for cta in (0, 57):
     t0 = min(v for v in (r[512], r[0]) if v > 0)
     f = lambda v: f"{(v - t0) / 1e3:7.2f}" if v > 0 else "      -"
     print(f"CTA {cta}: tile done at {f(r[1000])} us")
-    print("  kb  tma-issue  pfull  xexp-empty  xexp-full  wexp-full  mma-got")
+    print("  kb  tma-issue  pfull  xexp-empty  xexp-full  wexp-full  mma-got (stage = kb // 2 for M <= 32)")
     for kb in list(range(0, 12)) + list(range(28, 36)) + list(range(56, 64)):
         print(f"  {kb:2d}  {f(r[512 + kb // 4]) if kb % 4 == 0 else '       '}  "
-              f"{f(r[128 + kb // 4]) if kb % 4 == 0 else '       '}  {f(r[256 + kb])}  {f(r[384 + kb])}  "
-              f"{f(r[640 + kb])}  {f(r[kb])}")
+              f"{f(r[128 + kb // 4]) if kb % 4 == 0 else '       '}  "
+              f"{f(r[256 + kb])}  {f(r[384 + kb])}  {f(r[640 + kb // 2])}  {f(r[kb // 2])}")
