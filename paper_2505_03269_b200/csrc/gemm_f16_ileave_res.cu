@@ -40,8 +40,13 @@ constexpr int X_BOX = 64 * BK * 2;     // one TMA box: 64 real columns x 64 k-ro
 constexpr int X_HALF = 2 * X_BOX;      // one 128-row MMA half of a slot
 constexpr int X_SLOT = 2 * X_HALF;     // 32 KB
 constexpr int W_TILE = BB * BK * 2;    // one weight plane (8 KB)
-constexpr int W_STAGE = 2 * W_TILE;    // [W_r ; W_i]
-constexpr int W_STAGES = 6;
+constexpr int W_BLK = 2 * W_TILE;      // [W_r ; W_i] of one 64-k block
+// Two K blocks per weight stage: the MMA issuer waits and commits once per 16 MMAs.  Every wait or
+// commit between MMA issues idles the tensor pipe for a few hundred cycles
+// (tools/probes/mma_pattern_probe.cu), against ~630 cycles of tensor work per block at N = 128.
+constexpr int W_SBLK = 2;
+constexpr int W_STAGE = W_SBLK * W_BLK;
+constexpr int W_STAGES = 3;
 constexpr int EPI_WARPS = 8;
 constexpr int LOADER_WARP = 2 + EPI_WARPS;
 constexpr int NUM_THREADS = (LOADER_WARP + 1) * 32;
@@ -131,15 +136,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         for (int mt = 0; mt < tiles_m; ++mt) {
-          for (int kb = 0; kb < num_kb; ++kb) {
+          for (int kb0 = 0; kb0 < num_kb; kb0 += W_SBLK) {
+            const int nb = min(W_SBLK, num_kb - kb0);
             mbar_wait(&wempty[stage], phase ^ 1);
             uint8_t* st = sW + stage * W_STAGE;
-            mbar_arrive_expect_tx(&wfull[stage], W_STAGE);
-            if (MC) {
-              tma_load_3d_mc(st + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
-            } else {
-              tma_load_3d(st, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
-              tma_load_3d(st + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+            mbar_arrive_expect_tx(&wfull[stage], nb * W_BLK);
+            for (int j = 0; j < nb; ++j) {
+              const int kb = kb0 + j;
+              if (MC) {
+                tma_load_3d_mc(st + j * W_BLK + rank * W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + rank);
+              } else {
+                tma_load_3d(st + j * W_BLK, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b);
+                tma_load_3d(st + j * W_BLK + W_TILE, &tmW, &wfull[stage], kb * BK, mt * BB, 2 * b + 1);
+              }
             }
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -160,23 +169,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + abuf * 4 * BB;  // two halves of 2 BB columns
-        for (int kb = 0; kb < num_kb; ++kb) {
-          if (mt == 0) mbar_wait(&xfull[kb], ui & 1);  // the unit's data slot has landed
+        for (int kb0 = 0; kb0 < num_kb; kb0 += W_SBLK) {
+          const int nb = min(W_SBLK, num_kb - kb0);
+          if (mt == 0) {  // the unit's data slots have landed
+            mbar_wait(&xfull[kb0], ui & 1);
+            if (nb > 1) mbar_wait(&xfull[kb0 + 1], ui & 1);
+          }
           mbar_wait(&wfull[stage], phase);
           tc_fence_after();
-          const uint64_t w0 = desc_w(sW + stage * W_STAGE, 0);
-          const uint64_t x0 = desc_x(sX + kb * X_SLOT, 0), x1 = desc_x(sX + kb * X_SLOT + X_HALF, 0);
           if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {  // K advance: +32 bytes = +2 in the address field
-              const uint32_t acc = (kb | kk) ? 1u : 0u;
-              if (TCBF_ABLATE(args, 2)) continue;
-              mma_f16_ss(d, x0 + (uint64_t)(kk * 128), w0 + (uint64_t)(kk * 2), IDESC, acc);          // samples 0..63
-              mma_f16_ss(d + 2 * BB, x1 + (uint64_t)(kk * 128), w0 + (uint64_t)(kk * 2), IDESC, acc); // 64..127
+            for (int j = 0; j < W_SBLK; ++j) {
+              if (j >= nb) break;
+              const int kb = kb0 + j;
+              const uint64_t w0 = desc_w(sW + stage * W_STAGE + j * W_BLK, 0);
+              const uint64_t x0 = desc_x(sX + kb * X_SLOT, 0), x1 = desc_x(sX + kb * X_SLOT + X_HALF, 0);
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {  // K advance: +32 bytes = +2 in the address field
+                const uint32_t acc = (kb | kk) ? 1u : 0u;
+                if (TCBF_ABLATE(args, 2)) continue;
+                mma_f16_ss(d, x0 + (uint64_t)(kk * 128), w0 + (uint64_t)(kk * 2), IDESC, acc);          // samples 0..63
+                mma_f16_ss(d + 2 * BB, x1 + (uint64_t)(kk * 128), w0 + (uint64_t)(kk * 2), IDESC, acc); // 64..127
+              }
+              if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data slot
             }
             if (MC) mma_commit_mc(&wempty[stage]);
             else mma_commit(&wempty[stage]);
-            if (mt == tiles_m - 1) mma_commit(&xempty[kb]);  // last reader of this data slot
           }
           __syncwarp();
           if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
