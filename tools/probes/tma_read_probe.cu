@@ -66,7 +66,7 @@ int main() {
   }
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  struct Case { int bw, br, stages, ctas; CUtensorMapSwizzle sw; CUtensorMapL2promotion pr; const char* name; };
+  struct Case { int bw, br, stages, ctas; CUtensorMapSwizzle sw; CUtensorMapL2promotion pr; const char* name; bool blocked = false; };
   const Case cases[] = {
       {32, 128, 3, 128, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "kernel today: 128 B x 128 rows, 3 deep"},
       {32, 128, 4, 128, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "128 B x 128 rows, 4 deep"},
@@ -76,12 +76,15 @@ int main() {
       {64, 64, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "256 B x 64 rows, 4 deep"},
       {128, 32, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "512 B x 32 rows, 4 deep"},
       {256, 16, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "1 KB x 16 rows, 4 deep"},
-      {32, 128, 4, 148, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "128 B x 128 rows, 4 deep, 148 CTAs (rows split)"},
+      {256, 16, 4, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "tile-blocked layout: contiguous 16 KB boxes, 4 deep", true},
+      {256, 16, 6, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, "tile-blocked layout: contiguous 16 KB boxes, 6 deep", true},
   };
   for (const Case& c : cases) {
     CUtensorMap tms[COPIES];
-    const cuuint64_t dims[3] = {(cuuint64_t)KW, (cuuint64_t)N, 2};
-    const cuuint64_t strides[2] = {(cuuint64_t)KW * 4, (cuuint64_t)N * KW * 4};
+    // blocked: each plane as [N * KW / 256][256] words, i.e. 1 KB rows; CTA c owns the contiguous
+    // rows of its tile (128 samples x KW words = 256 KB per plane) and reads them 16 rows at a time
+    const cuuint64_t dims[3] = {(cuuint64_t)(c.blocked ? 256 : KW), (cuuint64_t)(c.blocked ? (size_t)N * KW / 256 : N), 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)(c.blocked ? 1024 : KW * 4), (cuuint64_t)N * KW * 4};
     const cuuint32_t box[3] = {(cuuint32_t)c.bw, (cuuint32_t)c.br, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = CUDA_SUCCESS;
@@ -92,10 +95,11 @@ int main() {
     const int stage_bytes = 2 * c.bw * c.br * 4;
     const int smem = 1024 + c.stages * stage_bytes + 256;
     cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int rows_per_cta = c.ctas == 128 ? 128 : 112;  // 148 x 112 = 16576 >= N: the tail is OOB-filled
+    const int rows_per_cta = c.blocked ? 128 * KW / 256 : 128;
     int rot = 0;
     auto run = [&]() {
-      stream_kernel<<<c.ctas, 32, smem>>>(tms[rot++ % COPIES], KW, c.bw, c.br, c.stages, stage_bytes, rows_per_cta);
+      stream_kernel<<<c.ctas, 32, smem>>>(tms[rot++ % COPIES], c.blocked ? 256 : KW, c.bw, c.br, c.stages, stage_bytes,
+                                          rows_per_cta);
     };
     run();
     cudaError_t e = cudaDeviceSynchronize();
