@@ -1,6 +1,6 @@
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "f16i or ileave or next1" 2>&1 | tail -2
-for rep in 1 2 3; do
-for L in build/libtcbf_base.so paper_2505_03269_b200/lib/libtcbf.so; do
-  echo "== $L"
-  AB_LIB=$L AB_VARIANTS="f16i:,smaj:" python tools/ab_fused.py 1024 1024 256 256 200 2>&1 | grep -E "^f16i|^smaj" | head -4
-done; done
+for rep in 1 2; do
+python bench.py --config m32_b1_16384 --steps 100 --warmup 5 --no-cpu-baseline --no-energy --records "" 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('new', d['config']['gemm_ms'])"
+cp paper_2505_03269_b200/lib/libtcbf.so /tmp/new.so; cp build/libtcbf_head.so paper_2505_03269_b200/lib/libtcbf.so
+python bench.py --config m32_b1_16384 --steps 100 --warmup 5 --no-cpu-baseline --no-energy --records "" 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('head', d['config']['gemm_ms'])"
+cp /tmp/new.so paper_2505_03269_b200/lib/libtcbf.so
+done
