@@ -583,6 +583,21 @@ def test_b1_small_m_swapped_kernel_bit_exact(tcbf, shape):
     assert np.array_equal(y, oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B))
 
 
+@pytest.mark.parametrize("shape", [(32, 20000, 700, 2), (20, 9000, 520, 3), (32, 19000, 1024, 2), (64, 9000, 700, 3)])
+def test_b1_swapped_kernel_many_tiles_per_cta_bit_exact(tcbf, shape):
+    """More 128-sample tiles than SMs, so every CTA runs several: the 32-beam kernel's single
+    accumulator (the next tile's MMAs wait for the epilogue's TMEM loads) and its two-K-block
+    stages across tile boundaries, with an odd K-block count (a virtual block pads the last stage:
+    K = 700 / 520 -> 3 blocks) and an even one; and the 64-beam kernel (double-buffered)."""
+    M, N, K, B = shape
+    w = synth.generate("adc", 47, 0, B, M, K)
+    x = synth.generate("adc", 47, 1, B, K, N)
+    plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
+    assert "swap" in plan.variant
+    assert B * ((N + 127) // 128) > 148
+    assert np.array_equal(y, oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B))
+
+
 @pytest.mark.parametrize("shape", [(32, 300, 700, 2), (200, 260, 500, 1)])
 def test_b1_forced_swap64_bit_exact(tcbf, shape, monkeypatch):
     """TCBF_B1_SWAP=64 (experiment override): the swapped kernel with 64-beam tiles for any M,
