@@ -235,7 +235,7 @@ RAW_SHAPES = [
 ]
 
 
-@pytest.fixture(params=["auto", "force_stream", "beam_major", "beam_major_no_mc", "smaj_4epi"])
+@pytest.fixture(params=["auto", "force_stream", "beam_major", "beam_major_no_mc"])
 def raw_mode(request, monkeypatch):
     if request.param == "force_stream":   # small-M shapes through the streaming-conversion kernel
         monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
@@ -243,8 +243,6 @@ def raw_mode(request, monkeypatch):
         monkeypatch.setenv("TCBF_F16_FUSED", "beam")
     if request.param == "beam_major_no_mc":      # ... without the CTA-pair weight multicast
         monkeypatch.setenv("TCBF_F16_MC", "0")
-    if request.param == "smaj_4epi":             # sample-major kernel with 4 epilogue warps
-        monkeypatch.setenv("TCBF_SMAJ_EPI", "4")
     return request.param
 
 
@@ -758,6 +756,15 @@ def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
     """BASELINE configs[2]: M=1024, K=512, N=4096, batch=256."""
     _full_size(tcbf, "b1", 1024, 4096, 512, 256, "phase", "adc", synth.SEED_BASE + 2,
                batches=[0, 200, 255], rows=[0, 63, 64, 777, 1023])
+
+
+def test_full_size_radio_f16_raw_sampled(tcbf):
+    """BASELINE configs[1] through tcbf_beamform_raw, the launch bench.py times (sample-major
+    fused kernel, 2048 units on 148 CTAs)."""
+    plan = tcbf.Plan(1024, 1024, 256, 256, "f16")
+    assert plan.raw_variant == "f16_tcgen05_fused_smaj_128x128", plan.raw_variant
+    _full_size(tcbf, "f16", 1024, 1024, 256, 256, "phase", "adc", synth.SEED_BASE + 1,
+               batches=[0, 77, 255], rows=[0, 63, 64, 127, 128, 700, 1023], path="raw")
 
 
 def test_full_size_square_16384_sampled(tcbf):
