@@ -1,0 +1,461 @@
+// gemm_f16_tmem.cu -- sample-major fused 16-bit beamformer with the unit's DATA resident in TENSOR
+// memory and the NEXT unit's data staged in shared memory: fp32 data in, fp32 beams out.
+//
+// Same arithmetic as the other 16-bit kernels (fp16 RNE inputs, exact products, fp32 accumulation
+// in TMEM, four real sub-products per K step -- PAPER.md:143-159), computed transposed,
+//     D^T[n][m] = sum_k X[k][n] W[m][k],
+// with the data X (lane = sample) as the A operand read from TMEM and the weights as the K-major
+// B operand streamed through shared memory, stacked [W_r ; W_i] for 64 beams:
+//     [Re | Im] += X_r [W_r ; W_i]^T     (M=128, N=128, A from TMEM)
+//     Re        += X_i (-W_i)^T          (N=64, negate-B bit: the paper's negation step)
+//     Im        += X_i W_r^T             (N=64)
+//
+// Why ("data in tensor memory"): the shared-memory-resident sample-major kernel
+// (gemm_f16_smaj.cu) stalls ~7 us at every unit switch -- all of the next unit's fp32 data is
+// loaded behind the epilogue's output stores only once the last beam tile has released the
+// resident slots, because shared memory has no room for look-ahead beside three weight stages.
+// Here the resident unit lives in TMEM (256 columns: X_r, X_i for K16 <= 256), so shared memory
+// holds the NEXT unit's converted data (128 KB) beside the weight ring: the converters convert it
+// while the current unit runs, and at the switch only copy it into TMEM (tcgen05.st, ~32 KB per
+// 64-K block) as each block is released.  The fp32 data comes in by TMA (16-row boxes through a
+// 2-slot raw ring), not by converter ld.global: the loads no longer queue behind the epilogue's
+// output stores in the SM's load/store pipeline.  TMEM: data 0..255, two accumulators
+// [Re 64 | Im 64] at 256 and 384.  Issued from a converged warp, M=128 N=64 MMAs with A from TMEM
+// run at the full fp16 rate (peaks.cu kind 6: 1988 TFLOP/s; 1412 with single-lane issue).
+//
+// Roles: warp 0 TMA producer (weights), warp 1 MMA issuer, warps 2..9 epilogue (tcgen05.ld ->
+// coalesced 128-byte line stores, lane = sample), warps 10..17 converters, warp 18 TMA producer
+// (raw fp32 data).
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tcbf {
+namespace {
+
+constexpr int UN = 128;                     // samples per unit (MMA M, TMEM lanes)
+constexpr int BNB = 64;                     // beams per tile
+constexpr int BK = 64;                      // K per data block / per 128-byte weight row
+constexpr int KMAX = 256;                   // resident K (TMEM columns 0..255)
+constexpr int W_PLANE = BNB * BK * 2;       // 8 KB: 64 beams x 128 B
+constexpr int W_ATOM = 2 * W_PLANE;         // [W_r ; W_i] for one K block (the stacked N=128 operand)
+constexpr int EPI_WARPS = 8;
+constexpr int CONV_WARPS = 8;
+constexpr int CONV0 = 2 + EPI_WARPS;
+constexpr int RAW_WARP = CONV0 + CONV_WARPS;
+constexpr int NUM_THREADS = (RAW_WARP + 1) * 32;
+#ifndef TCBF_TMEM_RAW_ROWS
+#define TCBF_TMEM_RAW_ROWS 16
+#endif
+#ifndef TCBF_TMEM_WHINT
+#define TCBF_TMEM_WHINT 0
+#endif
+constexpr int RAW_ROWS = TCBF_TMEM_RAW_ROWS;     // k-rows per raw fp32 box
+constexpr int RAW_BYTES = RAW_ROWS * UN * 8;     // 16 rows x 128 complex samples: 16 KB
+constexpr int RAW_SLOTS = 2;
+constexpr int STG_BLOCK = 2 * 8 * UN * 16;      // staged fp16 of one 64-K block: [plane][k group of 8][sample] x 16 B
+constexpr int OFF_STG = 0;
+constexpr int OFF_W = (KMAX / BK) * STG_BLOCK;   // 128 KB of staging
+constexpr int W_BYTES = 224 * 1024 - OFF_W - RAW_SLOTS * RAW_BYTES;  // weight ring: the rest (64 KB)
+constexpr int OFF_RAW = OFF_W + W_BYTES;
+constexpr int BAR_OFFSET = OFF_RAW + RAW_SLOTS * RAW_BYTES;
+constexpr int SMEM_BYTES = 1024 + BAR_OFFSET + 256;
+constexpr uint32_t X_COL = 0;                // X_r columns [0,128), X_i [128,256)
+constexpr uint32_t ACC_COL = 256;            // accumulators [256,384), [384,512)
+static_assert(SMEM_BYTES <= 232448, "smem budget");
+
+// D[tmem] (+)= A[tmem] . B[smem]^T, kind::f16
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// K-major weights (B operand): 128-byte swizzle, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t desc_w(const void* tile) {
+  uint64_t d = (uint64_t)((smem_u32(tile) >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+// kind::f16: fp16 A/B, fp32 D, A from TMEM, B K-major, M = 128; bit 14 negates B
+__host__ __device__ constexpr uint32_t idesc_t(uint32_t N, bool negate_b) {
+  return (1u << 4) | ((negate_b ? 1u : 0u) << 14) | ((N >> 3) << 17) | ((uint32_t)(UN >> 4) << 24);
+}
+
+__device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                                 int32_t c1, int32_t c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t h2u(float lo, float hi) {
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// LAYOUT: 0 interleaved fp32 source [B][K][N] x (re, im), 1 planar [B][2][K][N]; WKB: K blocks per
+// weight stage (64 KB of weight ring: 4 / WKB stages)
+template <int LAYOUT, int WKB>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    cgemm_f16_tmem_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                          GemmF16Args args) {
+  constexpr int W_STAGE = WKB * W_ATOM;
+  constexpr int W_STAGES = W_BYTES / W_STAGE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sStg = smem + OFF_STG;
+  uint8_t* sW = smem + OFF_W;
+  uint8_t* sRaw = smem + OFF_RAW;
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + BAR_OFFSET);
+  uint64_t* wempty = wfull + W_STAGES;
+  uint64_t* xfull = wempty + W_STAGES;   // [KMAX / BK]: the unit's block is in TMEM
+  uint64_t* xempty = xfull + KMAX / BK;  // [KMAX / BK]: the unit's last tile has read it
+  uint64_t* tfull = xempty + KMAX / BK;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* rfull = tempty + 2;          // [RAW_SLOTS]: raw fp32 box landed
+  uint64_t* rempty = rfull + RAW_SLOTS;  // [RAW_SLOTS]: converters have read it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + RAW_SLOTS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_kb = args.num_kb;    // K16 / 64 <= 4
+  const int num_ws = (num_kb + WKB - 1) / WKB;  // weight stages per tile
+  const int tiles_m = args.tiles_m;  // 64-beam tiles
+  const int tiles_n = args.tiles_n;  // 128-sample units per batch entry
+  const int num_units = args.B * tiles_n;
+  const int M = args.M, N = args.N;
+  const int nraw = args.K16 / RAW_ROWS;  // raw boxes per unit
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W_STAGES; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
+    }
+    for (int s = 0; s < KMAX / BK; ++s) {
+      mbar_init(&xfull[s], CONV_WARPS);  // every converter warp writes part of each block
+      mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], EPI_WARPS);
+    }
+    for (int s = 0; s < RAW_SLOTS; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], CONV_WARPS);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer: weight stages of
+    // WKB K blocks, each block's [W_r ; W_i] contiguous (the stacked N = 128 operand)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+#if TCBF_TMEM_WHINT
+      uint64_t wpol;  // keep the weights (re-read by every unit of the batch entry) in L2
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(wpol));
+#endif
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int b = u / tiles_n;
+        for (int mt = 0; mt < tiles_m; ++mt) {
+          for (int ws = 0; ws < num_ws; ++ws) {
+            mbar_wait(&wempty[stage], phase ^ 1);
+            uint8_t* st = sW + stage * W_STAGE;
+            const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
+            mbar_arrive_expect_tx(&wfull[stage], nkb * W_ATOM);
+            for (int j = 0; j < nkb; ++j) {
+              const int kb = ws * WKB + j;
+#if TCBF_TMEM_WHINT
+              tma_load_3d_hint(st + j * W_ATOM, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b, wpol);
+              tma_load_3d_hint(st + j * W_ATOM + W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b + 1, wpol);
+#else
+              tma_load_3d(st + j * W_ATOM, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b);
+              tma_load_3d(st + j * W_ATOM + W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b + 1);
+#endif
+            }
+            if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (converged warp, one
+    // elected lane issues)
+    constexpr uint32_t I128 = idesc_t(2 * BNB, false);
+    constexpr uint32_t I64 = idesc_t(BNB, false);
+    constexpr uint32_t I64_NEGB = idesc_t(BNB, true);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, ui = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+      const uint32_t xphase = ui & 1;
+      for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+        const int abuf = it & 1;
+        unsigned long long* const trace = it < 128 ? args.trace : nullptr;  // dev timeline (tools/trace_smaj.py)
+        const unsigned long long tw0 = trace ? gtimer() : 0;
+        mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        unsigned long long wwait = 0, xwait = 0;
+        if (trace && lane == 0) {
+          stamp(trace, 4 * it);
+          stamp_val(trace, 512 + 4 * it + 3, gtimer() - tw0);
+        }
+        const uint32_t d_re = tmem_base + ACC_COL + abuf * 2 * BNB;  // [Re | Im]: 128 columns
+        const uint32_t d_im = d_re + BNB;
+        for (int ws = 0; ws < num_ws; ++ws) {
+          const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
+          const unsigned long long a0 = trace ? gtimer() : 0;
+          if (mt == 0)
+            for (int j = 0; j < nkb; ++j) mbar_wait(&xfull[ws * WKB + j], xphase);  // block in TMEM
+          const unsigned long long a1 = trace ? gtimer() : 0;
+          mbar_wait(&wfull[stage], phase);
+          if (trace) {
+            xwait += a1 - a0;
+            wwait += gtimer() - a1;
+          }
+          tc_fence_after();
+          const uint8_t* st = sW + stage * W_STAGE;
+          const uint64_t w0 = desc_w(st);
+          if (elect_one()) {
+            for (int j = 0; j < nkb; ++j) {
+              const int kb = ws * WKB + j;
+#pragma unroll
+              for (int kk = 0; kk < BK / 16; ++kk) {
+                // 16 K: 8 TMEM columns of the data, 32 B of the K-major weights (+2)
+                const uint32_t xc = X_COL + (uint32_t)(kb * BK + kk * 16) / 2;
+                const uint32_t xr = tmem_base + xc, xi = tmem_base + xc + KMAX / 2;
+                const uint64_t wri = w0 + (uint64_t)((j * W_ATOM) >> 4) + (uint64_t)(2 * kk);  // [W_r ; W_i]
+                const uint64_t wi = wri + (uint64_t)(W_PLANE >> 4);                               // W_i
+                const uint32_t acc = (kb | kk) ? 1u : 0u;
+                if (TCBF_ABLATE(args, 2)) continue;
+                mma_f16_ts(d_re, xr, wri, I128, acc);     // [Re | Im] += X_r [W_r ; W_i]^T
+                mma_f16_ts(d_re, xi, wi, I64_NEGB, 1u);   // Re += X_i (-W_i)^T
+                mma_f16_ts(d_im, xi, wri, I64, 1u);       // Im += X_i W_r^T
+              }
+            }
+            mma_commit(&wempty[stage]);
+            if (mt == tiles_m - 1)
+              for (int j = 0; j < nkb; ++j) mma_commit(&xempty[ws * WKB + j]);  // last reader of the block
+          }
+          __syncwarp();
+          if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (elect_one()) mma_commit(&tfull[abuf]);
+        __syncwarp();
+        if (trace && lane == 0) {
+          stamp(trace, 4 * it + 1);
+          stamp_val(trace, 512 + 4 * it, wwait);
+          stamp_val(trace, 512 + 4 * it + 1, xwait);
+        }
+      }
+    }
+  } else if (warp < CONV0) {
+    // ------------------------------------------------------------ epilogue: coalesced line stores
+    const int q = warp & 3;           // TMEM lane quadrant = samples 32q..32q+31 of the unit
+    const int half = (warp - 2) / 4;  // half 0 stores Re, half 1 Im
+    int it = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      const int b = u / tiles_n;
+      const int n = (u - b * tiles_n) * UN + q * 32 + lane;  // this thread's sample
+      const bool n_ok = n < N;
+      for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+        const int abuf = it & 1;
+        mbar_wait(&tfull[abuf], (it >> 1) & 1);
+        tc_fence_after();
+        unsigned long long* const trace = it < 128 ? args.trace : nullptr;
+        if (threadIdx.x == 64) stamp(trace, 4 * it + 2);
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ACC_COL + abuf * 2 * BNB + half * BNB;
+        uint32_t v[2][32];
+        tmem_ld_32x32b_x32(tb, v[0]);
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          tmem_wait_ld();
+          if (ch == 0) {
+            tmem_ld_32x32b_x32(tb + 32, v[1]);
+          } else {  // all TMEM reads of this tile complete: release the buffer
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[abuf]);
+          }
+          if (TCBF_ABLATE(args, 1)) continue;
+          const int mb = mt * BNB + ch * 32;
+          const uint32_t* vv = v[ch];
+          if (n_ok) {
+            float* col = args.out + ((size_t)(2 * b + half) * M + mb) * (size_t)N + n;
+            if (mb + 32 <= M) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) col[(size_t)j * N] = __uint_as_float(vv[j]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (mb + j < M) col[(size_t)j * N] = __uint_as_float(vv[j]);
+            }
+          }
+        }
+        if (trace && lane == 0) {
+          if (warp == 2) stamp(trace, 4 * it + 3);
+          if (warp == 1 + EPI_WARPS) stamp(trace, 512 + 4 * it + 2);
+        }
+      }
+    }
+  } else if (warp < RAW_WARP) {
+    // ------------------------------------------------------------ converters: a unit's raw fp32
+    // boxes -> fp16 staging while the previous unit runs in TMEM, then the staging -> TMEM block by
+    // block as the previous unit's last tile releases it
+    const int ct = threadIdx.x - CONV0 * 32;  // 0..255
+    const int cs = ct & (UN - 1);             // conversion: sample, and 8-row group of each raw box
+    const int ch = RAW_ROWS == 16 ? ct >> 7 : 0;
+    const bool conv_active = RAW_ROWS == 16 || ct < UN;  // 8-row boxes: half the threads convert
+    const int q = warp & 3;                   // copy: warp w may access TMEM lanes 32 (w % 4) ..
+    const int s = q * 32 + lane;              // copy: this thread's sample (TMEM lane)
+    const int half = (warp - CONV0) >> 2;     // copy: K rows [32 half, 32 half + 32) of each block
+    uint4* const stg = reinterpret_cast<uint4*>(sStg);  // [kb][plane][k group of 8][sample]
+    int rs = 0;
+    uint32_t rphase = 0;
+    int ui = 0;
+    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+      // 1) convert: box r holds k-rows RAW_ROWS r ..; this thread's 8 rows = k group (RAW_ROWS / 8) r + ch
+      static_assert(RAW_ROWS == 16 || RAW_ROWS == 8, "raw box rows");
+      for (int r = 0; r < nraw; ++r) {
+        mbar_wait(&rfull[rs], rphase);
+        const float* raw = reinterpret_cast<const float*>(sRaw + rs * RAW_BYTES);
+        float re[8], im[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (!conv_active) break;
+          const int row = ch * 8 + j;
+          if (LAYOUT == 0) {
+            const float2 f = reinterpret_cast<const float2*>(raw)[row * UN + cs];
+            re[j] = f.x; im[j] = f.y;
+          } else {
+            re[j] = raw[row * UN + cs];
+            im[j] = raw[(RAW_ROWS + row) * UN + cs];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[rs]);
+        if (++rs == RAW_SLOTS) { rs = 0; rphase ^= 1; }
+        if (TCBF_ABLATE(args, 4)) {  // ablation: data values ignored (timing only)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) re[j] = im[j] = 0.f;
+        }
+        if (!conv_active) continue;
+        const int g = (RAW_ROWS / 8) * r + ch;  // global k group (8 rows)
+        const int kb = g >> 3;
+        stg[((kb * 2 + 0) * 8 + (g & 7)) * UN + cs] =
+            make_uint4(h2u(re[0], re[1]), h2u(re[2], re[3]), h2u(re[4], re[5]), h2u(re[6], re[7]));
+        stg[((kb * 2 + 1) * 8 + (g & 7)) * UN + cs] =
+            make_uint4(h2u(im[0], im[1]), h2u(im[2], im[3]), h2u(im[4], im[5]), h2u(im[6], im[7]));
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CONV_WARPS * 32) : "memory");  // staging complete
+      // 2) at the switch: each block into TMEM once the previous unit's last tile has read it
+      for (int kb = 0; kb < num_kb; ++kb) {
+        uint32_t pr[16], pi[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 r4 = stg[((kb * 2 + 0) * 8 + 4 * half + c) * UN + s];
+          const uint4 i4 = stg[((kb * 2 + 1) * 8 + 4 * half + c) * UN + s];
+          pr[4 * c] = r4.x; pr[4 * c + 1] = r4.y; pr[4 * c + 2] = r4.z; pr[4 * c + 3] = r4.w;
+          pi[4 * c] = i4.x; pi[4 * c + 1] = i4.y; pi[4 * c + 2] = i4.z; pi[4 * c + 3] = i4.w;
+        }
+        mbar_wait(&xempty[kb], (ui & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t ta = tmem_base + ((uint32_t)(q * 32) << 16) + X_COL + (uint32_t)(kb * BK + half * 32) / 2;
+        tmem_st_32x32b_x16(ta, pr);
+        tmem_st_32x32b_x16(ta + KMAX / 2, pi);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xfull[kb]);
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(CONV_WARPS * 32) : "memory");  // staging read: reusable
+    }
+  } else {
+    // ------------------------------------------------------------ TMA producer: raw fp32 data boxes
+    // (16 k-rows x 128 samples; rows >= K and samples >= N are zero-filled)
+    if (lane == 0) {
+      int rs = 0;
+      uint32_t rphase = 0;
+      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+        const int b = u / tiles_n;
+        const int n0 = (u - b * tiles_n) * UN;
+        for (int r = 0; r < nraw; ++r) {
+          mbar_wait(&rempty[rs], rphase ^ 1);
+          uint8_t* dst = sRaw + rs * RAW_BYTES;
+          mbar_arrive_expect_tx(&rfull[rs], RAW_BYTES);
+          if (LAYOUT == 0) {
+            tma_load_3d(dst, &tmX, &rfull[rs], 2 * n0, r * RAW_ROWS, b);
+          } else {
+            tma_load_3d(dst, &tmX, &rfull[rs], n0, r * RAW_ROWS, 2 * b);
+            tma_load_3d(dst + RAW_BYTES / 2, &tmX, &rfull[rs], n0, r * RAW_ROWS, 2 * b + 1);
+          }
+          if (++rs == RAW_SLOTS) { rs = 0; rphase ^= 1; }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace
+
+bool gemm_f16_tmem_supported(int64_t K16) { return K16 <= KMAX; }
+int gemm_f16_tmem_beams() { return BNB; }
+int gemm_f16_tmem_raw_rows() { return RAW_ROWS; }
+
+// args: tiles_m = 64-beam tiles, tiles_n = 128-sample units per batch entry, num_kb = K16 / 64;
+// weights tensor map: box {64 K, 64 beam rows} per plane, 128-byte swizzle; data tensor map:
+// interleaved {2N floats, K, B} box {256, 16}, planar {N, K, 2B} box {128, 16}, no swizzle
+cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
+                                 int layout, int wkb, int num_sms, cudaStream_t stream) {
+  auto kern = layout == 0 ? (wkb == 2 ? cgemm_f16_tmem_kernel<0, 2> : cgemm_f16_tmem_kernel<0, 1>)
+                          : (wkb == 2 ? cgemm_f16_tmem_kernel<1, 2> : cgemm_f16_tmem_kernel<1, 1>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int units = args.B * args.tiles_n;
+  const int grid = units < num_sms ? units : num_sms;
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmW, tmX, args);
+  return cudaGetLastError();
+}
+
+}  // namespace tcbf

@@ -64,6 +64,13 @@ cudaError_t launch_gemm_f16_ileave_res(const CUtensorMap& tmW, const CUtensorMap
                                        int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_smaj(const CUtensorMap& tmW, const GemmF16Args& args, const float* x_src, int layout,
                                  int K, int cluster, int num_sms, cudaStream_t stream);
+// data-in-TMEM sample-major fused kernel (gemm_f16_tmem.cu): tiles_m = 64-beam tiles, tiles_n =
+// 128-sample units per batch entry, num_kb = K16 / 64 (K16 <= 256)
+bool gemm_f16_tmem_supported(int64_t K16);
+int gemm_f16_tmem_beams();
+int gemm_f16_tmem_raw_rows();
+cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
+                                 int layout, int wkb, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);

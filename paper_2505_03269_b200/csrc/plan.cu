@@ -205,15 +205,21 @@ void choose_kernels(tcbf_plan* p) {
   p->raw_mode = TCBF_RAW_PACK;
   // fused kernel kind: sample-major (coalesced line stores straight from TMEM, any N) by default;
   // the beam-major TMA-store kernel (needs N % 4 == 0) stays selectable for comparison
-  p->f16_fused_kind = TCBF_FUSED_SMAJ;
-  if (const char* e = getenv("TCBF_F16_FUSED"))
+  // (default: data resident in TMEM, next unit staged in smem; TCBF_F16_FUSED=smaj keeps the data
+  // in smem, =beam the beam-major TMA-store kernel)
+  p->f16_fused_kind = TCBF_FUSED_TMEM;
+  if (const char* e = getenv("TCBF_F16_FUSED")) {
     if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
+    else if (strcmp(e, "smaj") == 0) p->f16_fused_kind = TCBF_FUSED_SMAJ;
+  }
+  p->tmem_wkb = env_int("TCBF_TMEM_WKB", 1) == 2 ? 2 : 1;  // K blocks per weight stage
   // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
   p->smaj_cluster = p->f16_multicast ? 2 : 1;
   p->f16i_resident = tcbf::gemm_f16_ileave_res_supported(p->kp) && !env_set("TCBF_F16I_STREAM");
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
-    const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ ? tcbf::gemm_f16_smaj_supported(p->kp)
-                                                              : tcbf::gemm_f16_fused_supported(p->kp, p->N);
+    const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ   ? tcbf::gemm_f16_smaj_supported(p->kp)
+                         : p->f16_fused_kind == TCBF_FUSED_TMEM ? tcbf::gemm_f16_tmem_supported(p->kp)
+                                                                : tcbf::gemm_f16_fused_supported(p->kp, p->N);
     if (fusable) {
       p->raw_mode = TCBF_RAW_FUSED;
     } else if (p->M <= 128 && p->N % 4 == 0) {
@@ -483,8 +489,9 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
     case TCBF_ENTRY_BEAMFORM: return gemm_kernel_name(plan);
     case TCBF_ENTRY_BEAMFORM_RAW:
       if (plan->raw_mode == TCBF_RAW_FUSED)
-        return plan->f16_fused_kind == TCBF_FUSED_SMAJ ? "f16_tcgen05_fused_smaj_128x128"
-                                                       : "f16_tcgen05_fused_pack_bres_128x128";
+        return plan->f16_fused_kind == TCBF_FUSED_SMAJ   ? "f16_tcgen05_fused_smaj_128x128"
+               : plan->f16_fused_kind == TCBF_FUSED_TMEM ? "f16_tcgen05_fused_tmem_128x64"
+                                                         : "f16_tcgen05_fused_pack_bres_128x128";
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
@@ -545,7 +552,61 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_SMAJ) {
+  // data-in-TMEM kernel: its raw fp32 data comes in by TMA, which needs 16-byte row strides and base
+  // (interleaved: N even; planar: N % 4 == 0); other calls take the sample-major kernel
+  const bool tmem_tma_ok = aligned(x_src, 16) && (layout == TCBF_SRC_INTERLEAVED ? plan->N % 2 == 0 : plan->N % 4 == 0);
+  if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_TMEM && tmem_tma_ok) {
+    // weights: the stacked K-major B operand, boxes {64 K, 64 beams} of a plane, 128-byte swizzle
+    CUtensorMap tw, tx;
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 64,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    const uint32_t rr = (uint32_t)tcbf::gemm_f16_tmem_raw_rows();
+    if (layout == TCBF_SRC_INTERLEAVED)
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x_src, 2 * plan->N, plan->K, plan->B, 256, rr,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    else
+      s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, x_src, plan->N, plan->K, 2 * plan->B, 128, rr,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    const int bn = tcbf::gemm_f16_tmem_beams();
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + bn - 1) / bn);  // 64-beam tiles
+    a.tiles_n = (int)((plan->N + 127) / 128);    // 128-sample units per batch entry
+    a.num_kb = (int)(plan->kp / 64);
+    const int64_t nu = (int64_t)a.tiles_n * plan->B;
+    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
+    a.num_tiles = (int)(nu * a.tiles_m);
+    a.out = static_cast<float*>(out);
+    a.debug = plan->debug;
+#ifdef TCBF_DEV
+    const char* trace_file = getenv("TCBF_TRACE");  // dev timeline (tools/trace_smaj.py)
+    if (trace_file) {
+      cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
+      cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
+    }
+#endif
+    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, (int)layout, plan->tmem_wkb, plan->num_sms, st);
+#ifdef TCBF_DEV
+    if (trace_file) {
+      std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
+      cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      cudaFree(a.trace);
+      if (FILE* f = fopen(trace_file, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
+#endif
+    if (e != cudaSuccess) return cuda_fail(e, "fused (data in TMEM) beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
+  if (plan->raw_mode == TCBF_RAW_FUSED &&
+      (plan->f16_fused_kind == TCBF_FUSED_SMAJ || plan->f16_fused_kind == TCBF_FUSED_TMEM)) {
     // weights as the stacked K-major B operand: boxes {64 K, 64 beams} of a plane, 128-byte swizzle
     // (a stage is four boxes, split among the CTAs of a multicast cluster)
     CUtensorMap tw;

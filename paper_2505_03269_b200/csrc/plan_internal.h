@@ -11,7 +11,7 @@
 
 enum { TCBF_B1K_POPC = 0, TCBF_B1K_I8 = 1, TCBF_B1K_F4 = 4, TCBF_B1K_BMMA = 5 };
 enum { TCBF_RAW_PACK = 0, TCBF_RAW_FUSED = 1, TCBF_RAW_STREAM = 2 };
-enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_BEAM_MAJOR = 1 };
+enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_BEAM_MAJOR = 1, TCBF_FUSED_TMEM = 2 };
 
 struct tcbf_plan_s {
   int64_t M, N, K, B;
@@ -27,6 +27,7 @@ struct tcbf_plan_s {
   int f16_fused_kind; // TCBF_FUSED_*: which fused fp32-data kernel tcbf_beamform_raw runs
   int f16i_resident;  // tcbf_beamform_f16i: resident-data kernel (K16 <= 256) instead of the streaming one
   int smaj_cluster;   // sample-major fused kernel: weight-multicast cluster size (1 or 2)
+  int tmem_wkb;       // data-in-TMEM fused kernel: K blocks per weight stage (1 or 2)
   int raw_mode;       // TCBF_RAW_*: what tcbf_beamform_raw runs
   int conv_splits_override;  // streaming-conversion K split (0 = by shape)
   int b1_kernel;      // TCBF_B1K_*: fp4 +-1 tensor cores (default), int8 AND form, legacy b1 mma.sync, popc

@@ -235,7 +235,7 @@ RAW_SHAPES = [
 ]
 
 
-@pytest.fixture(params=["auto", "force_stream", "beam_major", "beam_major_no_mc"])
+@pytest.fixture(params=["auto", "force_stream", "beam_major", "beam_major_no_mc", "smaj"])
 def raw_mode(request, monkeypatch):
     if request.param == "force_stream":   # small-M shapes through the streaming-conversion kernel
         monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
@@ -243,6 +243,8 @@ def raw_mode(request, monkeypatch):
         monkeypatch.setenv("TCBF_F16_FUSED", "beam")
     if request.param == "beam_major_no_mc":      # ... without the CTA-pair weight multicast
         monkeypatch.setenv("TCBF_F16_MC", "0")
+    if request.param == "smaj":                  # sample-major kernel with the data resident in smem
+        monkeypatch.setenv("TCBF_F16_FUSED", "smaj")
     return request.param
 
 
@@ -259,7 +261,7 @@ def test_f16_beamform_raw_bitwise_equals_packed_path(tcbf, shape, raw_mode, monk
     y_raw = plan.beamform_raw(wp, xd, layout)
     y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
     torch.cuda.synchronize()
-    if "smaj" in plan.raw_variant:
+    if "smaj" in plan.raw_variant or "tmem" in plan.raw_variant:
         # sample-major kernel: the same fp16 products and fp32 accumulation, computed as X^T W^T
         # with an N=256 MMA -- the tensor core's in-MMA summation order differs by fp32 ulps
         assert (y_raw - y_ref).abs().max().item() <= 1e-6 * y_ref.abs().max().item()
@@ -759,12 +761,44 @@ def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
 
 
 def test_full_size_radio_f16_raw_sampled(tcbf):
-    """BASELINE configs[1] through tcbf_beamform_raw, the launch bench.py times (sample-major
-    fused kernel, 2048 units on 148 CTAs)."""
+    """BASELINE configs[1] through tcbf_beamform_raw, the launch bench.py times (data-in-TMEM fused
+    kernel: 2048 units on 148 CTAs, the data of each next unit staged in smem, raw data by TMA)."""
     plan = tcbf.Plan(1024, 1024, 256, 256, "f16")
-    assert plan.raw_variant == "f16_tcgen05_fused_smaj_128x128", plan.raw_variant
+    assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x64", plan.raw_variant
     _full_size(tcbf, "f16", 1024, 1024, 256, 256, "phase", "adc", synth.SEED_BASE + 1,
                batches=[0, 77, 255], rows=[0, 63, 64, 127, 128, 700, 1023], path="raw")
+
+
+# several 128-sample units per CTA (the staged next unit copied into TMEM at each switch), K16 =
+# 64 / 192 / 256 (1, 3, 4 data blocks; 4 .. 16 raw boxes per unit), ragged M and N, planar source,
+# and an odd N (interleaved rows not 16-byte strided: the call takes the smem sample-major kernel)
+TMEM_SHAPES = [
+    (130, 520, 200, 40, "interleaved"),
+    (64, 256, 64, 160, "planar"),
+    (200, 1000, 130, 30, "interleaved"),
+    (96, 333, 100, 20, "interleaved"),
+]
+
+
+@pytest.mark.parametrize("shape", TMEM_SHAPES)
+def test_f16_tmem_fused_kernel(tcbf, shape):
+    """The data-in-TMEM fused kernel equals pack + beamform up to fp32 summation order inside the
+    MMA and meets the oracle on sampled batch entries."""
+    M, N, K, B, layout = shape
+    w = synth.generate("phase", 37, 0, B, M, K)
+    x = synth.generate("adc", 37, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x64", plan.raw_variant
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
+    xd = _dev(conv(x))
+    y_raw = plan.beamform_raw(wp, xd, layout)
+    y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
+    torch.cuda.synchronize()
+    assert (y_raw - y_ref).abs().max().item() <= 1e-6 * y_ref.abs().max().item()
+    sel = sorted({0, B // 2, B - 1})
+    ref = oracle.cgemm_f16(conv(w[sel]), conv(x[sel]), 0 if layout == "interleaved" else 1, M, N, K, len(sel))
+    _check_f16(y_raw[sel].cpu().numpy(), ref, w[sel], x[sel])
 
 
 def test_full_size_square_16384_sampled(tcbf):
