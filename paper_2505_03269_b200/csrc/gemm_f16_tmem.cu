@@ -47,9 +47,20 @@ constexpr int EPI_WARPS = 8;
 constexpr int CONV_WARPS = 8;
 constexpr int CONV0 = 2 + EPI_WARPS;
 constexpr int RAW_WARP = CONV0 + CONV_WARPS;
-constexpr int NUM_THREADS = (RAW_WARP + 1) * 32;
+#ifndef TCBF_TMEM_SYNCWARP
+#define TCBF_TMEM_SYNCWARP 1
+#endif
+constexpr int SYNC_WARP = RAW_WARP + 1;  // TCBF_TMEM_SYNCWARP: waits on the MMA issuer's barriers for it
+constexpr int NUM_THREADS = (RAW_WARP + 1 + TCBF_TMEM_SYNCWARP) * 32;
+constexpr int NB_STAGE0 = 2;             // named barriers 2.. : weight stage s ready (sync warp -> MMA warp)
 #ifndef TCBF_TMEM_RAW_ROWS
 #define TCBF_TMEM_RAW_ROWS 16
+#endif
+#ifndef TCBF_TMEM_NOFENCE
+#define TCBF_TMEM_NOFENCE 0
+#endif
+#ifndef TCBF_TMEM_PEEK
+#define TCBF_TMEM_PEEK 0
 #endif
 #ifndef TCBF_TMEM_WHINT
 #define TCBF_TMEM_WHINT 0
@@ -118,7 +129,10 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
 
 // LAYOUT: 0 interleaved fp32 source [B][K][N] x (re, im), 1 planar [B][2][K][N]; WKB: K blocks per
 // weight stage (64 KB of weight ring: 4 / WKB stages)
-template <int LAYOUT, int WKB>
+// CL = 2: CTA pairs (clusters) take adjacent units of one batch entry and walk the same weight
+// stages; each CTA TMA-loads one plane of a stage and multicasts it into both (half the L2 -> SM
+// weight reads), a stage is refilled once the MMAs of both CTAs have retired it
+template <int LAYOUT, int WKB, int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     cgemm_f16_tmem_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                           GemmF16Args args) {
@@ -141,6 +155,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  constexpr bool MC = CL > 1;
+  const int rank = MC ? (int)cluster_ctarank() : 0;
+  const int u_first = MC ? CL * (int)(blockIdx.x / CL) + rank : (int)blockIdx.x;
+  const int u_step = MC ? CL * (int)(gridDim.x / CL) : (int)gridDim.x;
   const int num_kb = args.num_kb;    // K16 / 64 <= 4
   const int num_ws = (num_kb + WKB - 1) / WKB;  // weight stages per tile
   const int tiles_m = args.tiles_m;  // 64-beam tiles
@@ -152,7 +170,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < W_STAGES; ++s) {
       mbar_init(&wfull[s], 1);
-      mbar_init(&wempty[s], 1);
+      mbar_init(&wempty[s], CL);
     }
     for (int s = 0; s < KMAX / BK; ++s) {
       mbar_init(&xfull[s], CONV_WARPS);  // every converter warp writes part of each block
@@ -175,7 +193,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tmem_relinquish();
   }
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // the peer signals this CTA's barriers
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -189,16 +207,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint64_t wpol;  // keep the weights (re-read by every unit of the batch entry) in L2
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(wpol));
 #endif
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         for (int mt = 0; mt < tiles_m; ++mt) {
           for (int ws = 0; ws < num_ws; ++ws) {
             mbar_wait(&wempty[stage], phase ^ 1);
             uint8_t* st = sW + stage * W_STAGE;
             const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
+            if (TCBF_ABLATE(args, 8) && mt > 0) {  // ablation: weights once per unit (wrong values)
+              mbar_arrive(&wfull[stage]);
+              if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+              continue;
+            }
             mbar_arrive_expect_tx(&wfull[stage], nkb * W_ATOM);
             for (int j = 0; j < nkb; ++j) {
               const int kb = ws * WKB + j;
+              if (MC) {  // this CTA's plane of the pair's shared stage, into both CTAs
+                tma_load_3d_mc(st + j * W_ATOM + rank * W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB,
+                               2 * b + rank, (uint16_t)((1u << CL) - 1u));
+                continue;
+              }
 #if TCBF_TMEM_WHINT
               tma_load_3d_hint(st + j * W_ATOM, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b, wpol);
               tma_load_3d_hint(st + j * W_ATOM + W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b + 1, wpol);
@@ -221,14 +249,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, ui = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+    bool wready = false;
+    (void)wready;
+    for (int u = u_first; u < num_units; u += u_step, ++ui) {
       const uint32_t xphase = ui & 1;
       for (int mt = 0; mt < tiles_m; ++mt, ++it) {
         const int abuf = it & 1;
         unsigned long long* const trace = it < 128 ? args.trace : nullptr;  // dev timeline (tools/trace_smaj.py)
         const unsigned long long tw0 = trace ? gtimer() : 0;
+#if !TCBF_TMEM_SYNCWARP
         mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
+#endif
         unsigned long long wwait = 0, xwait = 0;
         if (trace && lane == 0) {
           stamp(trace, 4 * it);
@@ -239,15 +271,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int ws = 0; ws < num_ws; ++ws) {
           const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
           const unsigned long long a0 = trace ? gtimer() : 0;
-          if (mt == 0)
+#if TCBF_TMEM_SYNCWARP
+          // one named-barrier sync per stage: the sync warp has seen this stage's weights, and for a
+          // tile's first stage the free accumulator buffer and (first tile of a unit) the data blocks
+          asm volatile("bar.sync %0, 64;" ::"r"(NB_STAGE0 + stage) : "memory");
+          tc_fence_after();
+          const unsigned long long a1 = a0;
+#else
+          if (mt == 0) {
             for (int j = 0; j < nkb; ++j) mbar_wait(&xfull[ws * WKB + j], xphase);  // block in TMEM
+            tc_fence_after();  // TMEM written by the converters' tcgen05.st
+          }
           const unsigned long long a1 = trace ? gtimer() : 0;
+#if TCBF_TMEM_PEEK
+          if (!wready) mbar_wait(&wfull[stage], phase);
+#else
           mbar_wait(&wfull[stage], phase);
+#endif
+#endif  // TCBF_TMEM_SYNCWARP
           if (trace) {
             xwait += a1 - a0;
             wwait += gtimer() - a1;
           }
+#if !TCBF_TMEM_NOFENCE
           tc_fence_after();
+#endif
+          // (a TMA-filled weight stage needs no tcgen05 fence after its barrier wait)
+#if TCBF_TMEM_PEEK
+          {  // peek at the next stage now, so its wait overlaps this stage's MMA issue
+            const int ns = stage + 1 == W_STAGES ? 0 : stage + 1;
+            const uint32_t np = stage + 1 == W_STAGES ? phase ^ 1 : phase;
+            wready = mbar_try_wait(&wfull[ns], np);
+          }
+#endif
           const uint8_t* st = sW + stage * W_STAGE;
           const uint64_t w0 = desc_w(st);
           if (elect_one()) {
@@ -267,7 +323,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mma_f16_ts(d_im, xi, wri, I64, 1u);       // Im += X_i W_r^T
               }
             }
-            mma_commit(&wempty[stage]);
+            if (MC) mma_commit_mc(&wempty[stage], (uint16_t)((1u << CL) - 1u));  // free in both CTAs
+            else mma_commit(&wempty[stage]);
             if (mt == tiles_m - 1)
               for (int j = 0; j < nkb; ++j) mma_commit(&xempty[ws * WKB + j]);  // last reader of the block
           }
@@ -288,7 +345,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3;           // TMEM lane quadrant = samples 32q..32q+31 of the unit
     const int half = (warp - 2) / 4;  // half 0 stores Re, half 1 Im
     int it = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = u_first; u < num_units; u += u_step) {
       const int b = u / tiles_n;
       const int n = (u - b * tiles_n) * UN + q * 32 + lane;  // this thread's sample
       const bool n_ok = n < N;
@@ -300,12 +357,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (threadIdx.x == 64) stamp(trace, 4 * it + 2);
         const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + ACC_COL + abuf * 2 * BNB + half * BNB;
         uint32_t v[2][32];
-        tmem_ld_32x32b_x32(tb, v[0]);
+        const bool no_ld = TCBF_ABLATE(args, 16);  // ablation: no TMEM reads (stores of garbage)
+        if (!no_ld) tmem_ld_32x32b_x32(tb, v[0]);
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
-          tmem_wait_ld();
+          if (!no_ld) tmem_wait_ld();
           if (ch == 0) {
-            tmem_ld_32x32b_x32(tb + 32, v[1]);
+            if (!no_ld) tmem_ld_32x32b_x32(tb + 32, v[1]);
           } else {  // all TMEM reads of this tile complete: release the buffer
             tc_fence_before();
             __syncwarp();
@@ -347,7 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int rs = 0;
     uint32_t rphase = 0;
     int ui = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x, ++ui) {
+    for (int u = u_first; u < num_units; u += u_step, ++ui) {
       // 1) convert: box r holds k-rows RAW_ROWS r ..; this thread's 8 rows = k group (RAW_ROWS / 8) r + ch
       static_assert(RAW_ROWS == 16 || RAW_ROWS == 8, "raw box rows");
       for (int r = 0; r < nraw; ++r) {
@@ -404,13 +462,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(CONV_WARPS * 32) : "memory");  // staging read: reusable
     }
+#if TCBF_TMEM_SYNCWARP
+  } else if (warp == SYNC_WARP) {
+    // ------------------------------------------------------------ sync warp: the MMA issuer's mbarrier
+    // waits (each a bubble in its tensor-pipe issue stream), passed on by one named barrier per stage
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, ui = 0;
+    for (int u = u_first; u < num_units; u += u_step, ++ui) {
+      for (int mt = 0; mt < tiles_m; ++mt, ++it) {
+        for (int ws = 0; ws < num_ws; ++ws) {
+          const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
+          if (ws == 0) mbar_wait(&tempty[it & 1], ((it >> 1) & 1) ^ 1);
+          if (mt == 0)
+            for (int j = 0; j < nkb; ++j) mbar_wait(&xfull[ws * WKB + j], ui & 1);
+          mbar_wait(&wfull[stage], phase);
+          asm volatile("bar.arrive %0, 64;" ::"r"(NB_STAGE0 + stage) : "memory");
+          if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+#endif
   } else {
     // ------------------------------------------------------------ TMA producer: raw fp32 data boxes
     // (16 k-rows x 128 samples; rows >= K and samples >= N are zero-filled)
     if (lane == 0) {
       int rs = 0;
       uint32_t rphase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         const int n0 = (u - b * tiles_n) * UN;
         for (int r = 0; r < nraw; ++r) {
@@ -430,7 +509,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (MC) cluster_sync(); else __syncthreads();  // no CTA exits while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
@@ -446,16 +525,50 @@ int gemm_f16_tmem_raw_rows() { return RAW_ROWS; }
 // args: tiles_m = 64-beam tiles, tiles_n = 128-sample units per batch entry, num_kb = K16 / 64;
 // weights tensor map: box {64 K, 64 beam rows} per plane, 128-byte swizzle; data tensor map:
 // interleaved {2N floats, K, B} box {256, 16}, planar {N, K, 2B} box {128, 16}, no swizzle
-cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
-                                 int layout, int wkb, int num_sms, cudaStream_t stream) {
-  auto kern = layout == 0 ? (wkb == 2 ? cgemm_f16_tmem_kernel<0, 2> : cgemm_f16_tmem_kernel<0, 1>)
-                          : (wkb == 2 ? cgemm_f16_tmem_kernel<1, 2> : cgemm_f16_tmem_kernel<1, 1>);
+template <int LAYOUT, int WKB, int CL>
+cudaError_t launch_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args, int num_sms,
+                        cudaStream_t stream) {
+  auto kern = cgemm_f16_tmem_kernel<LAYOUT, WKB, CL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int units = args.B * args.tiles_n;
-  const int grid = units < num_sms ? units : num_sms;
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmW, tmX, args);
+  int grid = units < num_sms ? units : num_sms;
+  if (CL == 1) {
+    kern<<<grid, NUM_THREADS, SMEM_BYTES, stream>>>(tmW, tmX, args);
+    return cudaGetLastError();
+  }
+  grid = grid / CL * CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, tmW, tmX, args);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// cluster 2 (weight multicast) needs an even number of units per batch entry (a pair never spans
+// two entries) and at least two units
+cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
+                                 int layout, int wkb, int cluster, int num_sms, cudaStream_t stream) {
+  const bool pair = cluster >= 2 && args.tiles_n % 2 == 0 && args.B * args.tiles_n >= 2;
+#define TCBF_TMEM_LAUNCH(L, W) \
+  return pair ? launch_tmem<L, W, 2>(tmW, tmX, args, num_sms, stream) : launch_tmem<L, W, 1>(tmW, tmX, args, num_sms, stream)
+  if (layout == 0) {
+    if (wkb == 2) TCBF_TMEM_LAUNCH(0, 2);
+    TCBF_TMEM_LAUNCH(0, 1);
+  }
+  if (wkb == 2) TCBF_TMEM_LAUNCH(1, 2);
+  TCBF_TMEM_LAUNCH(1, 1);
+#undef TCBF_TMEM_LAUNCH
 }
 
 }  // namespace tcbf

@@ -70,7 +70,7 @@ bool gemm_f16_tmem_supported(int64_t K16);
 int gemm_f16_tmem_beams();
 int gemm_f16_tmem_raw_rows();
 cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
-                                 int layout, int wkb, int num_sms, cudaStream_t stream);
+                                 int layout, int wkb, int cluster, int num_sms, cudaStream_t stream);
 cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);

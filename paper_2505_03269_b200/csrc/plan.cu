@@ -588,7 +588,7 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
       cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
     }
 #endif
-    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, (int)layout, plan->tmem_wkb, plan->num_sms, st);
+    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, (int)layout, plan->tmem_wkb, plan->smaj_cluster, plan->num_sms, st);
 #ifdef TCBF_DEV
     if (trace_file) {
       std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);

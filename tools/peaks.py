@@ -34,10 +34,11 @@ KINDS = {
     9: ("tcgen05_mxf4_ss_n64", "tcgen05.mma kind::mxf4 block32 128x64x64, A and B from smem", 1.0),
     10: ("tcgen05_mxf4_ts_n128", "tcgen05.mma kind::mxf4 block32 128x128x64, A from TMEM", 1.0),
     11: ("tcgen05_f16_ts_n128", "tcgen05.mma kind::f16 128x128x16, A from TMEM", 1.0),
+    12: ("tcgen05_f16_ts_radio_step", "kind::f16 N=128 + N=64 (negate B) + N=64, A from TMEM (radio K step)", 1.0),
 }
 # iterations per warp / issuing thread: each launch runs ~5-50 ms
 ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000, 6: 80000, 7: 80000, 8: 80000, 9: 80000,
-         10: 80000, 11: 80000}
+         10: 80000, 11: 80000, 12: 40000}
 
 
 def clocks():
