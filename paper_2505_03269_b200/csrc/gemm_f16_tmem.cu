@@ -127,7 +127,8 @@ __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// LAYOUT: 0 interleaved fp32 source [B][K][N] x (re, im), 1 planar [B][2][K][N]; WKB: K blocks per
+// LAYOUT: 0 interleaved fp32 source [B][K][N] x (re, im), 1 planar [B][2][K][N], 2 interleaved fp16
+// [B][K][N] x (re, im) (tcbf_beamform_f16i: NEXT-1, no rounding on the way in); WKB: K blocks per
 // weight stage (64 KB of weight ring: 4 / WKB stages)
 // CL = 2: CTA pairs (clusters) take adjacent units of one batch entry and walk the same weight
 // stages; each CTA TMA-loads one plane of a stage and multicasts it into both (half the L2 -> SM
@@ -410,34 +411,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       static_assert(RAW_ROWS == 16 || RAW_ROWS == 8, "raw box rows");
       for (int r = 0; r < nraw; ++r) {
         mbar_wait(&rfull[rs], rphase);
-        const float* raw = reinterpret_cast<const float*>(sRaw + rs * RAW_BYTES);
-        float re[8], im[8];
+        uint4 pre, pim;  // this thread's 8 k-values of X_r and X_i as fp16
+        if (LAYOUT == 2) {  // fp16 (re, im) pairs: de-interleave with byte permutes, no rounding
+          const uint32_t* raw = reinterpret_cast<const uint32_t*>(sRaw + rs * RAW_BYTES);
+          uint32_t v[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (!conv_active) break;
-          const int row = ch * 8 + j;
-          if (LAYOUT == 0) {
-            const float2 f = reinterpret_cast<const float2*>(raw)[row * UN + cs];
-            re[j] = f.x; im[j] = f.y;
-          } else {
-            re[j] = raw[row * UN + cs];
-            im[j] = raw[(RAW_ROWS + row) * UN + cs];
+          for (int j = 0; j < 8; ++j) v[j] = conv_active ? raw[(ch * 8 + j) * UN + cs] : 0u;
+          pre = make_uint4(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410),
+                           __byte_perm(v[4], v[5], 0x5410), __byte_perm(v[6], v[7], 0x5410));
+          pim = make_uint4(__byte_perm(v[0], v[1], 0x7632), __byte_perm(v[2], v[3], 0x7632),
+                           __byte_perm(v[4], v[5], 0x7632), __byte_perm(v[6], v[7], 0x7632));
+        } else {
+          const float* raw = reinterpret_cast<const float*>(sRaw + rs * RAW_BYTES);
+          float re[8], im[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int row = ch * 8 + j;
+            if (!conv_active) {
+              re[j] = im[j] = 0.f;
+            } else if (LAYOUT == 0) {
+              const float2 f = reinterpret_cast<const float2*>(raw)[row * UN + cs];
+              re[j] = f.x; im[j] = f.y;
+            } else {
+              re[j] = raw[row * UN + cs];
+              im[j] = raw[(RAW_ROWS + row) * UN + cs];
+            }
           }
+          pre = make_uint4(h2u(re[0], re[1]), h2u(re[2], re[3]), h2u(re[4], re[5]), h2u(re[6], re[7]));
+          pim = make_uint4(h2u(im[0], im[1]), h2u(im[2], im[3]), h2u(im[4], im[5]), h2u(im[6], im[7]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[rs]);
         if (++rs == RAW_SLOTS) { rs = 0; rphase ^= 1; }
-        if (TCBF_ABLATE(args, 4)) {  // ablation: data values ignored (timing only)
-#pragma unroll
-          for (int j = 0; j < 8; ++j) re[j] = im[j] = 0.f;
-        }
+        if (TCBF_ABLATE(args, 4)) pre = pim = make_uint4(0u, 0u, 0u, 0u);  // ablation: data ignored (timing)
         if (!conv_active) continue;
         const int g = (RAW_ROWS / 8) * r + ch;  // global k group (8 rows)
         const int kb = g >> 3;
-        stg[((kb * 2 + 0) * 8 + (g & 7)) * UN + cs] =
-            make_uint4(h2u(re[0], re[1]), h2u(re[2], re[3]), h2u(re[4], re[5]), h2u(re[6], re[7]));
-        stg[((kb * 2 + 1) * 8 + (g & 7)) * UN + cs] =
-            make_uint4(h2u(im[0], im[1]), h2u(im[2], im[3]), h2u(im[4], im[5]), h2u(im[6], im[7]));
+        stg[((kb * 2 + 0) * 8 + (g & 7)) * UN + cs] = pre;
+        stg[((kb * 2 + 1) * 8 + (g & 7)) * UN + cs] = pim;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(CONV_WARPS * 32) : "memory");  // staging complete
       // 2) at the switch: each block into TMEM once the previous unit's last tile has read it
@@ -495,8 +506,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int r = 0; r < nraw; ++r) {
           mbar_wait(&rempty[rs], rphase ^ 1);
           uint8_t* dst = sRaw + rs * RAW_BYTES;
-          mbar_arrive_expect_tx(&rfull[rs], RAW_BYTES);
-          if (LAYOUT == 0) {
+          mbar_arrive_expect_tx(&rfull[rs], LAYOUT == 2 ? RAW_BYTES / 2 : RAW_BYTES);
+          if (LAYOUT == 2) {  // fp16 (re, im) pairs as 32-bit elements {N, K, B}
+            tma_load_3d(dst, &tmX, &rfull[rs], n0, r * RAW_ROWS, b);
+          } else if (LAYOUT == 0) {
             tma_load_3d(dst, &tmX, &rfull[rs], 2 * n0, r * RAW_ROWS, b);
           } else {
             tma_load_3d(dst, &tmX, &rfull[rs], n0, r * RAW_ROWS, 2 * b);
@@ -565,6 +578,10 @@ cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX,
   if (layout == 0) {
     if (wkb == 2) TCBF_TMEM_LAUNCH(0, 2);
     TCBF_TMEM_LAUNCH(0, 1);
+  }
+  if (layout == 2) {
+    if (wkb == 2) TCBF_TMEM_LAUNCH(2, 2);
+    TCBF_TMEM_LAUNCH(2, 1);
   }
   if (wkb == 2) TCBF_TMEM_LAUNCH(1, 2);
   TCBF_TMEM_LAUNCH(1, 1);

@@ -216,6 +216,11 @@ void choose_kernels(tcbf_plan* p) {
   // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
   p->smaj_cluster = p->f16_multicast ? 2 : 1;
   p->f16i_resident = tcbf::gemm_f16_ileave_res_supported(p->kp) && !env_set("TCBF_F16I_STREAM");
+  // fp16 interleaved data: the data-in-TMEM kernel where it applies (TCBF_F16I=res keeps the
+  // kernel that multiplies the interleaved tile as stored, TCBF_F16I_STREAM the streaming one)
+  p->f16i_tmem = tcbf::gemm_f16_tmem_supported(p->kp) && !env_set("TCBF_F16I_STREAM");
+  if (const char* e = getenv("TCBF_F16I"))
+    if (strcmp(e, "res") == 0) p->f16i_tmem = 0;
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
     const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ   ? tcbf::gemm_f16_smaj_supported(p->kp)
                          : p->f16_fused_kind == TCBF_FUSED_TMEM ? tcbf::gemm_f16_tmem_supported(p->kp)
@@ -496,6 +501,7 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
       return plan->prec != TCBF_PREC_F16 ? "none"
+             : plan->f16i_tmem     ? "f16_tcgen05_interleaved_tmem_128x64"
              : plan->f16i_resident ? "f16_tcgen05_interleaved_resident_128x64" : "f16_tcgen05_interleaved_smaj_64x128";
   }
   return "none";
@@ -766,6 +772,34 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (plan->f16i_tmem) {
+    // data-in-TMEM kernel with the fp16 pairs by TMA ({N, K, B} 32-bit elements, 16-row boxes),
+    // de-interleaved into the staged next unit (DESIGN.md §4 NEXT-1)
+    CUtensorMap tw, tx;
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 64,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_f16, plan->N, plan->K, plan->B, 128,
+                  (uint32_t)tcbf::gemm_f16_tmem_raw_rows(), CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    tcbf::GemmF16Args a;
+    memset(&a, 0, sizeof(a));
+    const int bn = tcbf::gemm_f16_tmem_beams();
+    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
+    a.tiles_m = (int)((plan->M + bn - 1) / bn);
+    a.tiles_n = (int)((plan->N + 127) / 128);
+    a.num_kb = (int)(plan->kp / 64);
+    const int64_t nu = (int64_t)a.tiles_n * plan->B;
+    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many tiles");
+    a.num_tiles = (int)(nu * a.tiles_m);
+    a.out = static_cast<float*>(out);
+    a.debug = plan->debug;
+    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, 2, plan->tmem_wkb, plan->smaj_cluster, plan->num_sms, st);
+    if (e != cudaSuccess) return cuda_fail(e, "interleaved-fp16 (data in TMEM) beamform kernel launch");
+    g_launches = 1;
+    return TCBF_OK;
+  }
   if (plan->f16i_resident) {
     // data resident per 128-sample unit, 64-beam tiles: weights box {64 K, 64 beams}; interleaved
     // data as a real [B][K][2N] fp16 matrix, boxes {64 columns, 64 k-rows} (128-byte swizzle)

@@ -26,6 +26,7 @@ struct tcbf_plan_s {
   int f16_multicast;  // beam-major fused kernel: weight tiles multicast across CTA pairs
   int f16_fused_kind; // TCBF_FUSED_*: which fused fp32-data kernel tcbf_beamform_raw runs
   int f16i_resident;  // tcbf_beamform_f16i: resident-data kernel (K16 <= 256) instead of the streaming one
+  int f16i_tmem;      // tcbf_beamform_f16i: the data-in-TMEM kernel (K16 <= 256), preferred over both
   int smaj_cluster;   // sample-major fused kernel: weight-multicast cluster size (1 or 2)
   int tmem_wkb;       // data-in-TMEM fused kernel: K blocks per weight stage (1 or 2)
   int raw_mode;       // TCBF_RAW_*: what tcbf_beamform_raw runs

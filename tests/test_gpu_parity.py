@@ -302,11 +302,18 @@ def test_f16_beamform_raw_split_k(tcbf, shape, splits, monkeypatch):
 
 # ------------------------------------------------------------------ fp16 interleaved data, no pack (NEXT-1)
 @pytest.mark.parametrize("shape", [(8, 64, 32, 2), (200, 300, 100, 3), (130, 136, 64, 3), (300, 1000, 480, 2),
-                                   (1024, 1024, 256, 2), (1000, 260, 333, 1), (64, 4, 16, 1)])
-def test_f16i_interleaved_fp16_beamform(tcbf, shape):
-    """tcbf_beamform_f16i on fp16 interleaved data (read as a real K x 2N matrix, Re/Im recombined
-    in the epilogue): within the 16-bit tolerance of the oracle on the same fp16 values, and equal
-    to the planar path up to one fp32 rounding."""
+                                   (1024, 1024, 256, 2), (1000, 260, 333, 1), (64, 4, 16, 1), (96, 520, 200, 90)])
+@pytest.mark.parametrize("kernel", ["default", "res", "stream"])
+def test_f16i_interleaved_fp16_beamform(tcbf, shape, kernel, monkeypatch):
+    """tcbf_beamform_f16i on fp16 interleaved data: the default data-in-TMEM kernel (pairs
+    de-interleaved into the staged unit), the resident kernel (TCBF_F16I=res: the interleaved tile
+    as a real K x 2N operand, Re/Im recombined in the epilogue) and the streaming one -- within the
+    16-bit tolerance of the oracle on the same fp16 values, and equal to the planar path up to one
+    fp32 rounding."""
+    if kernel == "res":
+        monkeypatch.setenv("TCBF_F16I", "res")
+    if kernel == "stream":
+        monkeypatch.setenv("TCBF_F16I_STREAM", "1")
     M, N, K, B = shape
     w = synth.generate("phase", 29, 0, B, M, K)
     x = synth.generate("adc", 29, 1, B, K, N)
@@ -345,10 +352,15 @@ def test_f16i_resident_equals_streaming(tcbf, shape, monkeypatch):
     w = synth.generate("phase", 31, 0, B, M, K)
     x = synth.to_interleaved(synth.generate("adc", 31, 1, B, K, N)).astype(np.float16)
     xd = torch.from_numpy(x).cuda()
+    monkeypatch.setenv("TCBF_F16I", "res")
     plan = tcbf.Plan(M, N, K, B, "f16")
     assert "resident" in plan.kernel("f16i")
     wp = plan.pack(tcbf.WEIGHTS, _dev(synth.to_interleaved(w)))
     y_res = plan.beamform_f16i(wp, xd)
+    monkeypatch.delenv("TCBF_F16I")
+    pt = tcbf.Plan(M, N, K, B, "f16")
+    assert pt.kernel("f16i") == "f16_tcgen05_interleaved_tmem_128x64", pt.kernel("f16i")
+    y_tmem = pt.beamform_f16i(wp, xd)
     monkeypatch.setenv("TCBF_F16I_STREAM", "1")
     ps = tcbf.Plan(M, N, K, B, "f16")
     assert "resident" not in ps.kernel("f16i")
@@ -356,6 +368,7 @@ def test_f16i_resident_equals_streaming(tcbf, shape, monkeypatch):
     torch.cuda.synchronize()
     scale = y_str.abs().max().item()
     assert (y_res - y_str).abs().max().item() <= 1e-6 * scale
+    assert (y_tmem - y_str).abs().max().item() <= 1e-6 * scale
 
 
 def test_f16i_errors(tcbf):
