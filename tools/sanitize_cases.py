@@ -81,10 +81,16 @@ CASES = {
         ("f16_fused_raw", "f16", 200, 300, 100, 3, "raw", None),
         ("f16_fused_raw_tiny", "f16", 8, 64, 32, 2, "raw", None),
         ("f16_fused_raw_multicast", "f16", 200, 256, 100, 3, "raw", None),
+        ("f16_tmem_multi_unit", "f16", 70, 256, 100, 80, "raw", None),
+        ("f16_tmem_odd_n_fallback", "f16", 70, 77, 40, 2, "raw", None),
+        ("f16_tmem_no_multicast", "f16", 130, 300, 200, 3, "raw", {"TCBF_F16_MC": "0"}),
+        ("f16_smaj_raw", "f16", 200, 300, 100, 3, "raw", {"TCBF_F16_FUSED": "smaj"}),
         ("f16_stream_conv", "f16", 32, 260, 700, 1, "raw", {"TCBF_FORCE_STREAM_CONV": "1"}),
         ("f16_stream_conv_split", "f16", 40, 128, 3000, 1, "raw", {"TCBF_FORCE_STREAM_CONV": "1"}),
-        ("f16_interleaved_resident", "f16", 200, 300, 100, 2, "f16i", None),
-        ("f16_interleaved_resident_mc", "f16", 130, 256, 200, 3, "f16i", None),
+        ("f16_interleaved_tmem", "f16", 200, 300, 100, 2, "f16i", None),
+        ("f16_interleaved_tmem_multi_unit", "f16", 64, 512, 64, 40, "f16i", None),
+        ("f16_interleaved_resident", "f16", 200, 300, 100, 2, "f16i", {"TCBF_F16I": "res"}),
+        ("f16_interleaved_resident_mc", "f16", 130, 256, 200, 3, "f16i", {"TCBF_F16I": "res"}),
         ("f16_interleaved_streaming", "f16", 200, 300, 100, 2, "f16i", {"TCBF_F16I_STREAM": "1"}),
         ("f16_interleaved_long_k", "f16", 100, 132, 333, 1, "f16i", None),
     ],
