@@ -132,11 +132,14 @@ def roofline_for(c, gemm_ms, peaks, long_step, variant="", fused=False):
     # fp16: 1x bf16; 1-bit on int8 MMAs (i8 / i8pair): 2x; on +-1 e4m3 (f8): 2x; on +-1 e2m1
     # with unit block scales (mxf4): 4x -- B200 nominal dense 2.25 / 4.5 / 4.5 / 9 P(FL)OP/s
     ratio = 1.0 if c["prec"] == "f16" else (4.0 if "mxf4" in variant else 2.0)
-    base = peaks["bf16_sus"] if long_step else peaks["bf16"]
+    # sustained = cuBLAS bf16 back to back at the board's power cap; the narrow-precision 1-bit
+    # kernels draw less power per op than that, so a long step of theirs keeps the burst base
+    # (x ratio) -- with the sustained base the fp4 planes workload read 1.13 of its "peak"
+    base = peaks["bf16_sus"] if (long_step and ratio == 1.0) else peaks["bf16"]
     tpeak = base * ratio
     t_hbm = byts / (bw * 1e9)
     t_tc = ops / (tpeak * 1e12)
-    src = peaks["src"] + (" sustained" if long_step else " burst") + {
+    src = peaks["src"] + (" sustained" if (long_step and ratio == 1.0) else " burst") + {
         1.0: "", 2.0: " x2 (int8/fp8 nominal ratio)", 4.0: " x4 (fp4 nominal ratio)"}[ratio]
     if t_hbm >= t_tc:
         # achieved = SURVEY.md §8(d)'s per-unit bytes as written (fp16: data counted at its packed
