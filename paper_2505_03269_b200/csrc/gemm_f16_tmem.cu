@@ -47,25 +47,10 @@ constexpr int EPI_WARPS = 8;
 constexpr int CONV_WARPS = 8;
 constexpr int CONV0 = 2 + EPI_WARPS;
 constexpr int RAW_WARP = CONV0 + CONV_WARPS;
-#ifndef TCBF_TMEM_SYNCWARP
-#define TCBF_TMEM_SYNCWARP 1
-#endif
-constexpr int SYNC_WARP = RAW_WARP + 1;  // TCBF_TMEM_SYNCWARP: waits on the MMA issuer's barriers for it
-constexpr int NUM_THREADS = (RAW_WARP + 1 + TCBF_TMEM_SYNCWARP) * 32;
+constexpr int SYNC_WARP = RAW_WARP + 1;  // waits on the MMA issuer's barriers for it
+constexpr int NUM_THREADS = (SYNC_WARP + 1) * 32;
 constexpr int NB_STAGE0 = 2;             // named barriers 2.. : weight stage s ready (sync warp -> MMA warp)
-#ifndef TCBF_TMEM_RAW_ROWS
-#define TCBF_TMEM_RAW_ROWS 16
-#endif
-#ifndef TCBF_TMEM_NOFENCE
-#define TCBF_TMEM_NOFENCE 0
-#endif
-#ifndef TCBF_TMEM_PEEK
-#define TCBF_TMEM_PEEK 0
-#endif
-#ifndef TCBF_TMEM_WHINT
-#define TCBF_TMEM_WHINT 0
-#endif
-constexpr int RAW_ROWS = TCBF_TMEM_RAW_ROWS;     // k-rows per raw fp32 box
+constexpr int RAW_ROWS = 16;                     // k-rows per raw data box (two 8-row halves)
 constexpr int RAW_BYTES = RAW_ROWS * UN * 8;     // 16 rows x 128 complex samples: 16 KB
 constexpr int RAW_SLOTS = 2;
 constexpr int STG_BLOCK = 2 * 8 * UN * 16;      // staged fp16 of one 64-K block: [plane][k group of 8][sample] x 16 B
@@ -111,15 +96,6 @@ __device__ __forceinline__ uint64_t desc_w(const void* tile) {
 // kind::f16: fp16 A/B, fp32 D, A from TMEM, B K-major, M = 128; bit 14 negates B
 __host__ __device__ constexpr uint32_t idesc_t(uint32_t N, bool negate_b) {
   return (1u << 4) | ((negate_b ? 1u : 0u) << 14) | ((N >> 3) << 17) | ((uint32_t)(UN >> 4) << 24);
-}
-
-__device__ __forceinline__ void tma_load_3d_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
-                                                 int32_t c1, int32_t c2, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
 }
 
 __device__ __forceinline__ uint32_t h2u(float lo, float hi) {
@@ -204,10 +180,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-#if TCBF_TMEM_WHINT
-      uint64_t wpol;  // keep the weights (re-read by every unit of the batch entry) in L2
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(wpol));
-#endif
       for (int u = u_first; u < num_units; u += u_step) {
         const int b = u / tiles_n;
         for (int mt = 0; mt < tiles_m; ++mt) {
@@ -228,13 +200,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                2 * b + rank, (uint16_t)((1u << CL) - 1u));
                 continue;
               }
-#if TCBF_TMEM_WHINT
-              tma_load_3d_hint(st + j * W_ATOM, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b, wpol);
-              tma_load_3d_hint(st + j * W_ATOM + W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b + 1, wpol);
-#else
               tma_load_3d(st + j * W_ATOM, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b);
               tma_load_3d(st + j * W_ATOM + W_PLANE, &tmW, &wfull[stage], kb * BK, mt * BNB, 2 * b + 1);
-#endif
             }
             if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
           }
@@ -250,18 +217,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, ui = 0;
-    bool wready = false;
-    (void)wready;
     for (int u = u_first; u < num_units; u += u_step, ++ui) {
       const uint32_t xphase = ui & 1;
       for (int mt = 0; mt < tiles_m; ++mt, ++it) {
         const int abuf = it & 1;
         unsigned long long* const trace = it < 128 ? args.trace : nullptr;  // dev timeline (tools/trace_smaj.py)
         const unsigned long long tw0 = trace ? gtimer() : 0;
-#if !TCBF_TMEM_SYNCWARP
-        mbar_wait(&tempty[abuf], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-#endif
         unsigned long long wwait = 0, xwait = 0;
         if (trace && lane == 0) {
           stamp(trace, 4 * it);
@@ -271,40 +232,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t d_im = d_re + BNB;
         for (int ws = 0; ws < num_ws; ++ws) {
           const int nkb = (num_kb - ws * WKB) < WKB ? (num_kb - ws * WKB) : WKB;
-          const unsigned long long a0 = trace ? gtimer() : 0;
-#if TCBF_TMEM_SYNCWARP
           // one named-barrier sync per stage: the sync warp has seen this stage's weights, and for a
           // tile's first stage the free accumulator buffer and (first tile of a unit) the data blocks
+          // in TMEM (an mbarrier wait in this issue stream costs the tensor pipe a ~300-cycle bubble
+          // even when the barrier is complete)
+          const unsigned long long a0 = trace ? gtimer() : 0;
           asm volatile("bar.sync %0, 64;" ::"r"(NB_STAGE0 + stage) : "memory");
-          tc_fence_after();
-          const unsigned long long a1 = a0;
-#else
-          if (mt == 0) {
-            for (int j = 0; j < nkb; ++j) mbar_wait(&xfull[ws * WKB + j], xphase);  // block in TMEM
-            tc_fence_after();  // TMEM written by the converters' tcgen05.st
-          }
-          const unsigned long long a1 = trace ? gtimer() : 0;
-#if TCBF_TMEM_PEEK
-          if (!wready) mbar_wait(&wfull[stage], phase);
-#else
-          mbar_wait(&wfull[stage], phase);
-#endif
-#endif  // TCBF_TMEM_SYNCWARP
-          if (trace) {
-            xwait += a1 - a0;
-            wwait += gtimer() - a1;
-          }
-#if !TCBF_TMEM_NOFENCE
-          tc_fence_after();
-#endif
-          // (a TMA-filled weight stage needs no tcgen05 fence after its barrier wait)
-#if TCBF_TMEM_PEEK
-          {  // peek at the next stage now, so its wait overlaps this stage's MMA issue
-            const int ns = stage + 1 == W_STAGES ? 0 : stage + 1;
-            const uint32_t np = stage + 1 == W_STAGES ? phase ^ 1 : phase;
-            wready = mbar_try_wait(&wfull[ns], np);
-          }
-#endif
+          tc_fence_after();  // the accumulator released by the epilogue, the data written by tcgen05.st
+          if (trace) wwait += gtimer() - a0;
           const uint8_t* st = sW + stage * W_STAGE;
           const uint64_t w0 = desc_w(st);
           if (elect_one()) {
@@ -397,8 +332,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // block as the previous unit's last tile releases it
     const int ct = threadIdx.x - CONV0 * 32;  // 0..255
     const int cs = ct & (UN - 1);             // conversion: sample, and 8-row group of each raw box
-    const int ch = RAW_ROWS == 16 ? ct >> 7 : 0;
-    const bool conv_active = RAW_ROWS == 16 || ct < UN;  // 8-row boxes: half the threads convert
+    const int ch = ct >> 7;
     const int q = warp & 3;                   // copy: warp w may access TMEM lanes 32 (w % 4) ..
     const int s = q * 32 + lane;              // copy: this thread's sample (TMEM lane)
     const int half = (warp - CONV0) >> 2;     // copy: K rows [32 half, 32 half + 32) of each block
@@ -407,8 +341,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t rphase = 0;
     int ui = 0;
     for (int u = u_first; u < num_units; u += u_step, ++ui) {
-      // 1) convert: box r holds k-rows RAW_ROWS r ..; this thread's 8 rows = k group (RAW_ROWS / 8) r + ch
-      static_assert(RAW_ROWS == 16 || RAW_ROWS == 8, "raw box rows");
+      // 1) convert: box r holds k-rows 16 r ..; this thread's 8 rows = k group 2 r + ch
       for (int r = 0; r < nraw; ++r) {
         mbar_wait(&rfull[rs], rphase);
         uint4 pre, pim;  // this thread's 8 k-values of X_r and X_i as fp16
@@ -416,7 +349,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t* raw = reinterpret_cast<const uint32_t*>(sRaw + rs * RAW_BYTES);
           uint32_t v[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = conv_active ? raw[(ch * 8 + j) * UN + cs] : 0u;
+          for (int j = 0; j < 8; ++j) v[j] = raw[(ch * 8 + j) * UN + cs];
           pre = make_uint4(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410),
                            __byte_perm(v[4], v[5], 0x5410), __byte_perm(v[6], v[7], 0x5410));
           pim = make_uint4(__byte_perm(v[0], v[1], 0x7632), __byte_perm(v[2], v[3], 0x7632),
@@ -427,9 +360,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int row = ch * 8 + j;
-            if (!conv_active) {
-              re[j] = im[j] = 0.f;
-            } else if (LAYOUT == 0) {
+            if (LAYOUT == 0) {
               const float2 f = reinterpret_cast<const float2*>(raw)[row * UN + cs];
               re[j] = f.x; im[j] = f.y;
             } else {
@@ -444,8 +375,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&rempty[rs]);
         if (++rs == RAW_SLOTS) { rs = 0; rphase ^= 1; }
         if (TCBF_ABLATE(args, 4)) pre = pim = make_uint4(0u, 0u, 0u, 0u);  // ablation: data ignored (timing)
-        if (!conv_active) continue;
-        const int g = (RAW_ROWS / 8) * r + ch;  // global k group (8 rows)
+        const int g = 2 * r + ch;  // global k group (8 rows)
         const int kb = g >> 3;
         stg[((kb * 2 + 0) * 8 + (g & 7)) * UN + cs] = pre;
         stg[((kb * 2 + 1) * 8 + (g & 7)) * UN + cs] = pim;
@@ -473,7 +403,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       asm volatile("bar.sync 1, %0;" ::"n"(CONV_WARPS * 32) : "memory");  // staging read: reusable
     }
-#if TCBF_TMEM_SYNCWARP
   } else if (warp == SYNC_WARP) {
     // ------------------------------------------------------------ sync warp: the MMA issuer's mbarrier
     // waits (each a bubble in its tensor-pipe issue stream), passed on by one named barrier per stage
@@ -493,7 +422,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-#endif
   } else {
     // ------------------------------------------------------------ TMA producer: raw fp32 data boxes
     // (16 k-rows x 128 samples; rows >= K and samples >= N are zero-filled)
