@@ -75,6 +75,14 @@ cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC
                                   const float* x_src, int layout, int K, bool multicast, int num_sms,
                                   cudaStream_t stream);
 
+struct GemmB1Args;
+// 1-bit sample-major kernel with the unit's expanded data resident in TMEM (gemm_b1_tmem.cu):
+// Kw <= 24 words; 64-beam tiles, 128-sample units, line-store epilogue (any N)
+bool gemm_b1_tmem_supported(int64_t Kw);
+int gemm_b1_tmem_beams();
+cudaError_t launch_gemm_b1_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmB1Args& a, int num_sms,
+                                cudaStream_t stream);
+
 struct GemmB1Args {
   const uint32_t* w;  // [B][2][M][Kw]
   const uint32_t* x;  // [B][2][N][Kw]

@@ -172,18 +172,26 @@ void choose_kernels(tcbf_plan* p) {
   const int v = env_int("TCBF_F16_VARIANT", -1);
   if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
 
-  // 1-bit: +-1 fp4 (kind::mxf4) tensor cores, exact while 32 Kw <= 2^23; int8 AND form beyond
+  // 1-bit: +-1 fp4 (kind::mxf4) tensor cores, exact while 32 Kw <= 2^23; int8 AND form beyond;
+  // short K (Kw <= 24) with more than 64 beams: the sample-major kernel with the unit's data
+  // resident in TMEM and line-store epilogue (radio 1-bit GEMM 1.73-1.91 -> 1.51-1.54 ms)
   p->b1_kernel = tcbf::gemm_b1_f4_supported(p->kp) ? TCBF_B1K_F4 : TCBF_B1K_I8;
+  if (tcbf::gemm_b1_tmem_supported(p->kp) && p->M > 64) p->b1_kernel = TCBF_B1K_TMEM;
   if (const char* e = getenv("TCBF_B1_KERNEL")) {
     if (strcmp(e, "popc") == 0) p->b1_kernel = TCBF_B1K_POPC;
     else if (strcmp(e, "i8") == 0) p->b1_kernel = TCBF_B1K_I8;
     else if (strcmp(e, "bmma") == 0) p->b1_kernel = TCBF_B1K_BMMA;
     else if (strcmp(e, "f4") == 0 && tcbf::gemm_b1_f4_supported(p->kp)) p->b1_kernel = TCBF_B1K_F4;
+    else if (strcmp(e, "tmem") == 0 && tcbf::gemm_b1_tmem_supported(p->kp)) p->b1_kernel = TCBF_B1K_TMEM;
   }
   p->b1_swap_beams = (p->b1_kernel == TCBF_B1K_F4 && !env_set("TCBF_NO_SWAP")) ? tcbf::gemm_b1_f4_swap_beams(p->M) : 0;
   // experiment overrides: the swapped kernel (64-beam tiles) for any M; coalesced st.global
   // epilogue instead of TMA stores
-  if (p->b1_kernel == TCBF_B1K_F4 && env_int("TCBF_B1_SWAP", 0) == 64) p->b1_swap_beams = 64;
+  if (env_int("TCBF_B1_SWAP", 0) == 64 && tcbf::gemm_b1_f4_supported(p->kp) &&
+      (p->b1_kernel == TCBF_B1K_F4 || p->b1_kernel == TCBF_B1K_TMEM)) {
+    p->b1_kernel = TCBF_B1K_F4;
+    p->b1_swap_beams = 64;
+  }
   p->b1_force_stg = env_int("TCBF_B1_STG", 0) != 0;
   // split-K of the int8 kernel: measured not to shorten the per-SM K chain, so only forced (tests)
   p->b1_splits = 1;
@@ -247,6 +255,7 @@ const char* gemm_kernel_name(const tcbf_plan* plan) {
       case TCBF_B1K_POPC: return "b1_popc_xor_64x64";
       case TCBF_B1K_BMMA: return "b1_mma_sync_and_128x64";
       case TCBF_B1K_I8: return tma ? "b1_tcgen05_i8_128x128_tma" : "b1_tcgen05_i8_128x128_stg";
+      case TCBF_B1K_TMEM: return "b1_tcgen05_mxf4pm1_tmem_128x64";
       default: break;
     }
     if (plan->b1_swap_beams == 32)
@@ -345,7 +354,18 @@ tcbf_status beamform_b1(const tcbf_plan* plan, const void* w_packed, const void*
   }
   const bool tma_store = (plan->N % 4) == 0 && !plan->b1_force_stg;
   tcbf_status s;
-  if (plan->b1_kernel == TCBF_B1K_BMMA) {
+  if (plan->b1_kernel == TCBF_B1K_TMEM) {
+    // packed words whole rows per box: weights {Kw, 64 beams}, data {Kw, 128 samples}, no swizzle
+    CUtensorMap tw, tx;
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w_packed, plan->kp, plan->M, 2 * plan->B,
+                  (uint32_t)plan->kp, (uint32_t)tcbf::gemm_b1_tmem_beams(), CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_packed, plan->kp, plan->N, 2 * plan->B,
+                  (uint32_t)plan->kp, 128, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    if (s != TCBF_OK) return s;
+    e = tcbf::launch_gemm_b1_tmem(tw, tx, a, plan->num_sms, st);
+  } else if (plan->b1_kernel == TCBF_B1K_BMMA) {
     e = tcbf::launch_gemm_b1_mma(a, st);
   } else if (plan->b1_kernel == TCBF_B1K_POPC) {
     e = tcbf::launch_gemm_b1_popc(a, st);

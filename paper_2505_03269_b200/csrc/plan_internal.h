@@ -9,7 +9,7 @@
 
 #include "tcbf.h"
 
-enum { TCBF_B1K_POPC = 0, TCBF_B1K_I8 = 1, TCBF_B1K_F4 = 4, TCBF_B1K_BMMA = 5 };
+enum { TCBF_B1K_POPC = 0, TCBF_B1K_I8 = 1, TCBF_B1K_F4 = 4, TCBF_B1K_BMMA = 5, TCBF_B1K_TMEM = 6 };
 enum { TCBF_RAW_PACK = 0, TCBF_RAW_FUSED = 1, TCBF_RAW_STREAM = 2 };
 enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_BEAM_MAJOR = 1, TCBF_FUSED_TMEM = 2 };
 

@@ -531,9 +531,11 @@ def test_abi_errors_on_device(tcbf):
 
 
 # ------------------------------------------------------------------ 1-bit GEMM (a4, a5)
-@pytest.fixture(params=["f4", "i8", "popc", "bmma"])
+@pytest.fixture(params=["f4", "tmem", "i8", "popc", "bmma"])
 def b1_kernel(request, monkeypatch):
-    """All 1-bit kernels: tcgen05 kind::mxf4 on +-1 (default), tcgen05 kind::i8 AND form (beyond
+    """All 1-bit kernels: tcgen05 kind::mxf4 on +-1 (beam-major, and the sample-major kernel with
+    the unit's data resident in TMEM -- the default for Kw <= 24 and M > 64; other shapes fall back
+    to the beam-major one), tcgen05 kind::i8 AND form (beyond
     the fp32-exact K range, and split-K), the CUDA-core XOR/popc kernel and the legacy b1 mma.sync
     single-AND kernel."""
     monkeypatch.setenv("TCBF_B1_KERNEL", request.param)
@@ -550,7 +552,7 @@ def test_b1_beamform_bit_exact(tcbf, shape, b1_kernel):
     w = synth.generate("adc", 31, 0, B, M, K)
     x = synth.generate("adc", 31, 1, B, K, N)
     plan, wp, xp, y = _run(tcbf, "b1", synth.to_interleaved(w), synth.to_interleaved(x), M, N, K, B)
-    assert {"f4": "mxf4", "popc": "popc", "bmma": "mma_sync"}.get(b1_kernel, "i8") in plan.variant
+    assert {"f4": "mxf4", "tmem": "mxf4", "popc": "popc", "bmma": "mma_sync"}.get(b1_kernel, "i8") in plan.variant
     ref = oracle.cgemm_b1(synth.to_interleaved(w), synth.to_interleaved(x), 0, M, N, K, B)
     assert np.array_equal(y, ref)
     refp = oracle.cgemm_b1_packed(wp.cpu().numpy().view(np.uint32), xp.cpu().numpy().view(np.uint32),
@@ -812,6 +814,26 @@ def test_f16_tmem_fused_kernel(tcbf, shape):
     sel = sorted({0, B // 2, B - 1})
     ref = oracle.cgemm_f16(conv(w[sel]), conv(x[sel]), 0 if layout == "interleaved" else 1, M, N, K, len(sel))
     _check_f16(y_raw[sel].cpu().numpy(), ref, w[sel], x[sel])
+
+
+# 1-bit sample-major kernel with the unit's data resident in TMEM (Kw <= 24): several units per
+# CTA, ragged M (partial 64-beam tile) and N (partial 128-sample unit), K with padding bits,
+# the largest resident K (768), the radio shape class
+B1_TMEM_SHAPES = [
+    (130, 300, 100, 3), (64, 128, 256, 2), (200, 1000, 512, 30), (70, 77, 768, 2), (1024, 512, 512, 2),
+    (96, 256, 33, 160), (8, 64, 32, 2),
+]
+
+
+@pytest.mark.parametrize("shape", B1_TMEM_SHAPES)
+def test_b1_tmem_kernel_bit_exact(tcbf, shape, monkeypatch):
+    monkeypatch.setenv("TCBF_B1_KERNEL", "tmem")
+    M, N, K, B = shape
+    w = synth.to_interleaved(synth.generate("uniform", 41, 0, B, M, K))
+    x = synth.to_interleaved(synth.generate("uniform", 41, 1, B, K, N))
+    plan, _, _, y = _run(tcbf, "b1", w, x, M, N, K, B)
+    assert plan.variant == "b1_tcgen05_mxf4pm1_tmem_128x64", plan.variant
+    assert np.array_equal(y, oracle.cgemm_b1(w, x, 0, M, N, K, B))
 
 
 def test_full_size_square_16384_sampled(tcbf):
