@@ -116,27 +116,28 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
  * w_packed / x_packed: buffers written by tcbf_pack (16-byte aligned);
  * out: tcbf_output_bytes() bytes, 16-byte aligned, must not overlap the inputs.
  * F16: fp32 result of fp16 inputs with fp32 accumulation (tcgen05 tensor cores).
- * B1:  exact int32 result (the packed bits are expanded to +-1 -- weights into tensor memory,
- *      data into shared memory -- and multiplied on the fp4 tensor cores, exact for K <= 2^23,
- *      int8 tensor cores beyond).
+ * B1:  exact int32 result (the packed bits are expanded to +-1 and multiplied on the fp4 tensor
+ *      cores, exact for K <= 2^23, int8 tensor cores beyond; for K <= 768 and
+ *      M > 64 each 128-sample unit's expanded data stays in tensor memory for all beam tiles).
  * One launch, or two (memset + kernel) when a split-K variant is forced.  One call may be in
  * flight per (plan, out) pair; the plan itself is stateless and may be used from several streams. */
 tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed,
                           void* out, void* stream);
 
 /* The beamformer straight from the fp32 data source (device pointer, `layout` as for
- * tcbf_pack): the data pack is fused into the GEMM where the shape allows it (F16 plans with
- * round_up(K, 64) <= 256 and N % 4 == 0: each data element is converted to fp16 once, inside
- * the GEMM, into a shared-memory-resident operand -- PAPER.md:414 future work, no separate
- * transpose/pack pass; F16 plans with M <= 128, N % 4 == 0 and a 16-byte aligned source: the
- * data streams through the GEMM once, staged by TMA, with the K range split across CTAs when
- * the column tiles leave SMs idle -- then the output is zeroed first (a memset launch) and
- * partial sums are added, so that case matches tcbf_pack + tcbf_beamform to fp32 summation
- * order rather than bit for bit).  Other plans pack into a stream-ordered scratch buffer
- * (cudaMallocAsync from the device's default pool, whose release threshold is raised so the
- * memory stays cached; ALLOC on failure) and call tcbf_beamform.  Otherwise results are
- * bit-identical to tcbf_pack(DATA) followed by tcbf_beamform.  Same pointer rules as
- * tcbf_beamform. */
+ * tcbf_pack): the data pack is fused into the GEMM where the shape allows it (PAPER.md:414
+ * future work, no separate transpose/pack pass).  F16 plans with round_up(K, 64) <= 256: each
+ * data element is converted to fp16 once, inside the GEMM -- with N % 4 == 0 and a 16-byte
+ * aligned source into TENSOR memory (raw data by TMA, the next 128-sample unit staged in shared
+ * memory), else into a shared-memory-resident operand.  F16 plans with M <= 128, N % 4 == 0 and
+ * a 16-byte aligned source: the data streams through the GEMM once, staged by TMA, with the K
+ * range split across CTAs when the column tiles leave SMs idle (then the output is zeroed first,
+ * a memset launch, and partial sums are added).  Other plans pack into a stream-ordered scratch
+ * buffer (cudaMallocAsync from the device's default pool, whose release threshold is raised so
+ * the memory stays cached; ALLOC on failure) and call tcbf_beamform, bit-identical to
+ * tcbf_pack(DATA) + tcbf_beamform; the fused kernels form the same fp16 products and add them in
+ * the same K order, equal to that path up to fp32 rounding inside the MMA (a few ulps).  Same
+ * pointer rules as tcbf_beamform. */
 tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const float* x_src,
                               tcbf_src_layout layout, void* out, void* stream);
 

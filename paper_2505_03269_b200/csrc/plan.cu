@@ -215,10 +215,13 @@ void choose_kernels(tcbf_plan* p) {
   // the beam-major TMA-store kernel (needs N % 4 == 0) stays selectable for comparison
   // (default: data resident in TMEM, next unit staged in smem; TCBF_F16_FUSED=smaj keeps the data
   // in smem, =beam the beam-major TMA-store kernel)
-  p->f16_fused_kind = TCBF_FUSED_TMEM;
+  // (the TMEM kernel takes the raw data by TMA: 16-byte rows need N % 4 == 0 in either layout;
+  // other N take the smem sample-major kernel, chosen here so the plan's kernel name holds)
+  p->f16_fused_kind = p->N % 4 == 0 ? TCBF_FUSED_TMEM : TCBF_FUSED_SMAJ;
   if (const char* e = getenv("TCBF_F16_FUSED")) {
     if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
     else if (strcmp(e, "smaj") == 0) p->f16_fused_kind = TCBF_FUSED_SMAJ;
+    else if (strcmp(e, "tmem") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_TMEM;
   }
   p->tmem_wkb = env_int("TCBF_TMEM_WKB", 1) == 2 ? 2 : 1;  // K blocks per weight stage
   // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
@@ -578,9 +581,10 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   tcbf_status s = check_device(plan);
   if (s != TCBF_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // data-in-TMEM kernel: its raw fp32 data comes in by TMA, which needs 16-byte row strides and base
-  // (interleaved: N even; planar: N % 4 == 0); other calls take the sample-major kernel
-  const bool tmem_tma_ok = aligned(x_src, 16) && (layout == TCBF_SRC_INTERLEAVED ? plan->N % 2 == 0 : plan->N % 4 == 0);
+  // data-in-TMEM kernel (plans with N % 4 == 0): its raw fp32 data comes in by TMA, which needs a
+  // 16-byte-aligned source; a source aligned only to 8 (interleaved) or 4 (planar) bytes takes the
+  // smem sample-major kernel
+  const bool tmem_tma_ok = aligned(x_src, 16);
   if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_TMEM && tmem_tma_ok) {
     // weights: the stacked K-major B operand, boxes {64 K, 64 beams} of a plane, 128-byte swizzle
     CUtensorMap tw, tx;

@@ -785,14 +785,20 @@ def test_full_size_radio_f16_raw_sampled(tcbf):
 
 
 # several 128-sample units per CTA (the staged next unit copied into TMEM at each switch), K16 =
-# 64 / 192 / 256 (1, 3, 4 data blocks; 4 .. 16 raw boxes per unit), ragged M and N, planar source,
-# and an odd N (interleaved rows not 16-byte strided: the call takes the smem sample-major kernel)
+# 64 / 192 / 256 (1, 3, 4 data blocks; 4 .. 16 raw boxes per unit), ragged M and N, planar source
 TMEM_SHAPES = [
     (130, 520, 200, 40, "interleaved"),
     (64, 256, 64, 160, "planar"),
     (200, 1000, 130, 30, "interleaved"),
-    (96, 333, 100, 20, "interleaved"),
+    (96, 332, 100, 20, "planar"),
 ]
+
+
+def test_f16_tmem_fused_kernel_odd_n_plan(tcbf):
+    """N % 4 != 0: the plan picks the smem sample-major fused kernel at creation (TMA rows need
+    16-byte strides), and the kernel name says so."""
+    assert tcbf.Plan(96, 333, 100, 2, "f16").raw_variant == "f16_tcgen05_fused_smaj_128x128"
+    assert tcbf.Plan(96, 332, 100, 2, "f16").raw_variant == "f16_tcgen05_fused_tmem_128x64"
 
 
 @pytest.mark.parametrize("shape", TMEM_SHAPES)
