@@ -95,3 +95,25 @@ def test_sharded_equals_unsharded_on_cuda():
                 ref_rows = oracle.cgemm_f16(w, x, 0, len(rows), N, K, 1)
                 err = np.linalg.norm(got_rows.astype(np.float64) - ref_rows)
                 assert err <= 2e-3 * np.linalg.norm(ref_rows), name
+
+
+def test_bench_two_ranks_strong_scaling_line():
+    """bench.py's N > 1 path end to end (the driver's torchrun launch, gloo, both ranks on cuda:0):
+    one JSON line from rank 0, the FIXED global radio batch split into two 128-channel slices
+    (strong scaling), timing reduced over ranks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--dist-backend", "gloo", "--config", "radio_f16", "--steps", "3", "--warmup", "3",
+           "--no-cpu-baseline", "--no-energy", "--records", ""]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["config"]["global_batch"] == 256 and d["config"]["batch_per_gpu"] == 128
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] >= 3
