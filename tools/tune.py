@@ -26,9 +26,11 @@ SHAPES = [  # name, prec, M, N, K, B, wdist, xdist
 ]
 # packed-operand GEMM variants (tcbf::F16_V_*): 1-CTA 128x128 BK32 / BK64, 1-CTA 128x64, CTA pairs
 F16_VARIANTS = {"1cta_k32s4e8": "0", "1cta_k64s3": "1", "1cta_n64": "2", "2cta_256x128": "3", "2cta_256x256": "4"}
-# 1-bit: fp4 (+-1 e2m1, weights in TMEM; the swapped small-M kernel for M <= 64), fp4 forced
+# 1-bit: fp4 resident-data TMEM kernel (short K), fp4 (+-1 e2m1, weights in TMEM; the swapped
+# small-M kernel for M <= 64), fp4 forced
 # unswapped / forced swapped, int8 AND form, legacy b1 mma.sync, CUDA-core popc
-B1_VARIANTS = {"f4": {"TCBF_B1_KERNEL": "f4"}, "f4_noswap": {"TCBF_B1_KERNEL": "f4", "TCBF_NO_SWAP": "1"},
+B1_VARIANTS = {"tmem": {"TCBF_B1_KERNEL": "tmem"},  # resident data in TMEM (default for Kw <= 24, M > 64)
+               "f4": {"TCBF_B1_KERNEL": "f4"}, "f4_noswap": {"TCBF_B1_KERNEL": "f4", "TCBF_NO_SWAP": "1"},
                "f4_swap64": {"TCBF_B1_KERNEL": "f4", "TCBF_B1_SWAP": "64"}, "i8": {"TCBF_B1_KERNEL": "i8"},
                "bmma": {"TCBF_B1_KERNEL": "bmma"}, "popc": {"TCBF_B1_KERNEL": "popc"}}
 
