@@ -80,8 +80,8 @@ tcbf_status tcbf_layout_sizes(int64_t M, int64_t N, int64_t K, int64_t batch,
  * set to NULL on failure.  The plan owns only host metadata.
  * The kernel every entry point will run is chosen here, from the shape (DESIGN.md §4 policy).
  * Experiment overrides are read from the environment HERE ONLY (TCBF_F16_VARIANT,
- * TCBF_B1_KERNEL=f4|i8|bmma|popc, TCBF_NO_SWAP, TCBF_B1_SWAP=64, TCBF_B1_STG, TCBF_B1_SPLITS,
- * TCBF_NO_FUSED, TCBF_F16_FUSED=beam, TCBF_FORCE_STREAM_CONV, TCBF_CONV_SPLITS, TCBF_F16_MC,
+ * TCBF_B1_KERNEL=tmem|f4|i8|bmma|popc, TCBF_NO_SWAP, TCBF_B1_SWAP=64, TCBF_B1_STG, TCBF_B1_SPLITS,
+ * TCBF_NO_FUSED, TCBF_F16_FUSED=smaj, TCBF_TMEM_WKB, TCBF_F16I=res, TCBF_FORCE_STREAM_CONV, TCBF_CONV_SPLITS, TCBF_F16_MC,
  * TCBF_PACK_WPT); every variant they
  * select computes the same result (1-bit: bit-exact; 16-bit: within the fp32 summation-order
  * tolerance), and a plan never reads the environment again. */

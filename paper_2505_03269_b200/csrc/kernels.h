@@ -44,7 +44,6 @@ cudaError_t launch_gemm_f16(const CUtensorMap& tmA, const CUtensorMap& tmB, cons
                             const GemmF16Args& args, int variant, int epi, int num_sms,
                             cudaStream_t stream);
 
-bool gemm_f16_fused_supported(int64_t K16, int64_t N);
 int gemm_f16_ileave_block_k();
 int gemm_f16_ileave_block_n();
 cudaError_t launch_gemm_f16_ileave(const CUtensorMap& tmA, const CUtensorMap& tmX, const CUtensorMap& tmC,
@@ -71,10 +70,6 @@ int gemm_f16_tmem_beams();
 int gemm_f16_tmem_raw_rows();
 cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
                                  int layout, int wkb, int cluster, int num_sms, cudaStream_t stream);
-cudaError_t launch_gemm_f16_fused(const CUtensorMap& tmA, const CUtensorMap& tmC, const GemmF16Args& args,
-                                  const float* x_src, int layout, int K, bool multicast, int num_sms,
-                                  cudaStream_t stream);
-
 struct GemmB1Args;
 // 1-bit sample-major kernel with the unit's expanded data resident in TMEM (gemm_b1_tmem.cu):
 // Kw <= 24 words; 64-beam tiles, 128-sample units, line-store epilogue (any N)

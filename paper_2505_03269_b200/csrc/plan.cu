@@ -219,8 +219,7 @@ void choose_kernels(tcbf_plan* p) {
   // other N take the smem sample-major kernel, chosen here so the plan's kernel name holds)
   p->f16_fused_kind = p->N % 4 == 0 ? TCBF_FUSED_TMEM : TCBF_FUSED_SMAJ;
   if (const char* e = getenv("TCBF_F16_FUSED")) {
-    if (strcmp(e, "beam") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_BEAM_MAJOR;
-    else if (strcmp(e, "smaj") == 0) p->f16_fused_kind = TCBF_FUSED_SMAJ;
+    if (strcmp(e, "smaj") == 0) p->f16_fused_kind = TCBF_FUSED_SMAJ;
     else if (strcmp(e, "tmem") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_TMEM;
   }
   p->tmem_wkb = env_int("TCBF_TMEM_WKB", 1) == 2 ? 2 : 1;  // K blocks per weight stage
@@ -233,9 +232,8 @@ void choose_kernels(tcbf_plan* p) {
   if (const char* e = getenv("TCBF_F16I"))
     if (strcmp(e, "res") == 0) p->f16i_tmem = 0;
   if (p->prec == TCBF_PREC_F16 && !no_fused) {
-    const bool fusable = p->f16_fused_kind == TCBF_FUSED_SMAJ   ? tcbf::gemm_f16_smaj_supported(p->kp)
-                         : p->f16_fused_kind == TCBF_FUSED_TMEM ? tcbf::gemm_f16_tmem_supported(p->kp)
-                                                                : tcbf::gemm_f16_fused_supported(p->kp, p->N);
+    const bool fusable = p->f16_fused_kind == TCBF_FUSED_TMEM ? tcbf::gemm_f16_tmem_supported(p->kp)
+                                                              : tcbf::gemm_f16_smaj_supported(p->kp);
     if (fusable) {
       p->raw_mode = TCBF_RAW_FUSED;
     } else if (p->M <= 128 && p->N % 4 == 0) {
@@ -517,9 +515,8 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
     case TCBF_ENTRY_BEAMFORM: return gemm_kernel_name(plan);
     case TCBF_ENTRY_BEAMFORM_RAW:
       if (plan->raw_mode == TCBF_RAW_FUSED)
-        return plan->f16_fused_kind == TCBF_FUSED_SMAJ   ? "f16_tcgen05_fused_smaj_128x128"
-               : plan->f16_fused_kind == TCBF_FUSED_TMEM ? "f16_tcgen05_fused_tmem_128x64"
-                                                         : "f16_tcgen05_fused_pack_bres_128x128";
+        return plan->f16_fused_kind == TCBF_FUSED_TMEM ? "f16_tcgen05_fused_tmem_128x64"
+                                                       : "f16_tcgen05_fused_smaj_128x128";
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
@@ -676,50 +673,6 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     }
 #endif
     if (e != cudaSuccess) return cuda_fail(e, "fused (sample-major) beamform kernel launch");
-    g_launches = 1;
-    return TCBF_OK;
-  }
-  if (plan->raw_mode == TCBF_RAW_FUSED) {
-    CUtensorMap ta, tc;
-    s = encode_3d(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 128,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-    if (s != TCBF_OK) return s;
-    s = encode_3d(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, plan->N, plan->M, 2 * plan->B, 32, 128,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE);
-    if (s != TCBF_OK) return s;
-    tcbf::GemmF16Args a;
-    memset(&a, 0, sizeof(a));
-    a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
-    a.tiles_m = (int)((plan->M + 127) / 128);
-    a.tiles_n = (int)((plan->N + 127) / 128);
-    a.num_kb = (int)(plan->kp / 64);
-    const int64_t nu = (int64_t)a.tiles_n * plan->B;
-    if (nu * a.tiles_m > INT32_MAX) return fail(TCBF_ERR_INVALID_ARG, "too many work units");
-    a.num_tiles = (int)(nu * a.tiles_m);
-    a.out = static_cast<float*>(out);
-    a.debug = plan->debug;
-#ifdef TCBF_DEV
-    const char* trace_file = getenv("TCBF_TRACE");  // dev timeline of the fused kernel
-    if (trace_file) {
-      cudaMalloc(&a.trace, (size_t)plan->num_sms * 1024 * 8);
-      cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
-    }
-#endif
-    cudaError_t e = tcbf::launch_gemm_f16_fused(ta, tc, a, x_src, (int)layout, (int)plan->K, plan->f16_multicast != 0,
-                                                plan->num_sms, st);
-#ifdef TCBF_DEV
-    if (trace_file) {
-      std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
-      cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      cudaFree(a.trace);
-      if (FILE* f = fopen(trace_file, "wb")) {
-        fwrite(h.data(), 8, h.size(), f);
-        fclose(f);
-      }
-    }
-#endif
-    if (e != cudaSuccess) return cuda_fail(e, "fused beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;
   }

@@ -11,7 +11,7 @@
 
 enum { TCBF_B1K_POPC = 0, TCBF_B1K_I8 = 1, TCBF_B1K_F4 = 4, TCBF_B1K_BMMA = 5, TCBF_B1K_TMEM = 6 };
 enum { TCBF_RAW_PACK = 0, TCBF_RAW_FUSED = 1, TCBF_RAW_STREAM = 2 };
-enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_BEAM_MAJOR = 1, TCBF_FUSED_TMEM = 2 };
+enum { TCBF_FUSED_SMAJ = 0, TCBF_FUSED_TMEM = 2 };
 
 struct tcbf_plan_s {
   int64_t M, N, K, B;
@@ -23,7 +23,7 @@ struct tcbf_plan_s {
   size_t w_bytes, x_bytes, out_bytes;
   // kernel choice (choose_kernels in plan.cu)
   int f16_variant;    // tcbf::F16_V_*
-  int f16_multicast;  // beam-major fused kernel: weight tiles multicast across CTA pairs
+  int f16_multicast;  // fused kernels: weight stages multicast across CTA pairs (TCBF_F16_MC=0: off)
   int f16_fused_kind; // TCBF_FUSED_*: which fused fp32-data kernel tcbf_beamform_raw runs
   int f16i_resident;  // tcbf_beamform_f16i: resident-data kernel (K16 <= 256) instead of the streaming one
   int f16i_tmem;      // tcbf_beamform_f16i: the data-in-TMEM kernel (K16 <= 256), preferred over both

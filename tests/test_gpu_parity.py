@@ -235,13 +235,11 @@ RAW_SHAPES = [
 ]
 
 
-@pytest.fixture(params=["auto", "force_stream", "beam_major", "beam_major_no_mc", "smaj"])
+@pytest.fixture(params=["auto", "force_stream", "no_mc", "smaj"])
 def raw_mode(request, monkeypatch):
     if request.param == "force_stream":   # small-M shapes through the streaming-conversion kernel
         monkeypatch.setenv("TCBF_FORCE_STREAM_CONV", "1")
-    if request.param.startswith("beam_major"):   # the beam-major TMA-store fused kernel
-        monkeypatch.setenv("TCBF_F16_FUSED", "beam")
-    if request.param == "beam_major_no_mc":      # ... without the CTA-pair weight multicast
+    if request.param == "no_mc":                 # the fused kernel without the CTA-pair weight multicast
         monkeypatch.setenv("TCBF_F16_MC", "0")
     if request.param == "smaj":                  # sample-major kernel with the data resident in smem
         monkeypatch.setenv("TCBF_F16_FUSED", "smaj")

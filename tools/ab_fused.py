@@ -23,8 +23,7 @@ elif os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCB
     from paper_2505_03269_b200 import build as _b
     tcbf.library_path = _b.build_tcbf(dev=True)
 
-VARIANTS = [("tmem", {}), ("smaj", {"TCBF_F16_FUSED": "smaj"}), ("beam", {"TCBF_F16_FUSED": "beam"}),
-            ("beam_nomc", {"TCBF_F16_FUSED": "beam", "TCBF_F16_MC": "0"})]
+VARIANTS = [("tmem", {}), ("tmem_nomc", {"TCBF_F16_MC": "0"}), ("smaj", {"TCBF_F16_FUSED": "smaj"})]
 if os.environ.get("AB_VARIANTS"):   # e.g. "smaj8:,nostore:TCBF_DEBUG=1,nomma:TCBF_DEBUG=2"
     VARIANTS = []
     for item in os.environ["AB_VARIANTS"].split(","):

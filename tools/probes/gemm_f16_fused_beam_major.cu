@@ -1,3 +1,7 @@
+// PARKED (round 2): the round-1 beam-major fused fp16 kernel (fp32 data converted into an smem-
+// resident operand, TMEM -> smem -> TMA-store epilogue).  Measured slower than the sample-major
+// kernels that replaced it (profiles/r02/tuning.md: 0.733 vs 0.689 ms sustained on radio fp16).
+// To try it: copy into csrc/ and wire its launch in plan.cu as before (git history).
 // gemm_f16_fused.cu -- 16-bit-mode beamformer GEMM that consumes the fp32 data directly
 // (the data pack of PAPER.md:107 fused into the GEMM; the direction of the paper's future work
 // "a matrix-matrix multiplication kernel that does not require this transpose").

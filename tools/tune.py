@@ -104,7 +104,6 @@ def main():
                 variants.append(("fused_raw (conversion inside the GEMM)", {}, "raw"))
                 if base.kernel("raw").startswith("f16_tcgen05_fused_tmem"):
                     variants.append(("fused_raw sample-major, data in smem", {"TCBF_F16_FUSED": "smaj"}, "raw"))
-                    variants.append(("fused_raw beam-major", {"TCBF_F16_FUSED": "beam"}, "raw"))
             if base.N % 4 == 0 and base.k_packed <= 256:
                 variants.append(("fp16 interleaved data, resident (NEXT-1)", {}, "f16i"))
                 variants.append(("fp16 interleaved data, streaming (NEXT-1)", {"TCBF_F16I_STREAM": "1"}, "f16i"))
