@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
     const int ew = warp - 1;
-    const int te = ew * 32 + lane;  // column handled for the column popcounts
     uint8_t* stg = epi_base + ew * 8192;
     int sbuf = 0;
     int it = 0;

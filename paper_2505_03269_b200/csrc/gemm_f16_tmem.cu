@@ -216,9 +216,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     constexpr uint32_t I64_NEGB = idesc_t(BNB, true);
     int stage = 0;
     uint32_t phase = 0;
-    int it = 0, ui = 0;
-    for (int u = u_first; u < num_units; u += u_step, ++ui) {
-      const uint32_t xphase = ui & 1;
+    int it = 0;
+    for (int u = u_first; u < num_units; u += u_step) {
       for (int mt = 0; mt < tiles_m; ++mt, ++it) {
         const int abuf = it & 1;
         unsigned long long* const trace = it < 128 ? args.trace : nullptr;  // dev timeline (tools/trace_smaj.py)
