@@ -789,6 +789,7 @@ TMEM_SHAPES = [
     (64, 256, 64, 160, "planar"),
     (200, 1000, 130, 30, "interleaved"),
     (96, 332, 100, 20, "planar"),
+    (64, 512, 128, 10, "interleaved"),
 ]
 
 
