@@ -899,3 +899,29 @@ def test_full_size_ultrasound_f16_sampled(tcbf):
     """BASELINE configs[3]: M=65536, K=8192, N=256, batch=8 (17 GB of packed weights)."""
     _full_size(tcbf, "f16", 65536, 256, 8192, 8, "phase_amp", "adc_scaled", synth.SEED_BASE + 3,
                batches=[0, 7], rows=[0, 4097, 65535])
+
+
+@pytest.mark.parametrize("prec,shape", [("f16", (1024, 1024, 256, 64)), ("b1", (1024, 4096, 512, 16)),
+                                        ("f16", (1000, 1020, 200, 50))])
+def test_tmem_kernels_deterministic(tcbf, prec, shape):
+    """Race canary for the TMEM kernels (compute-sanitizer is unavailable on this pool): the same
+    launch repeated must give bitwise identical output -- a hand-off bug in the unit-switch staging,
+    the weight ring or the TMEM accumulator double buffer would show up as run-to-run differences
+    (every sum is formed in a fixed order, so correct runs are bitwise reproducible)."""
+    M, N, K, B = shape
+    plan = tcbf.Plan(M, N, K, B, prec)
+    w = synth.generate_device("phase", 53, 0, B, M, K)
+    x = synth.generate_device("adc", 53, 1, B, K, N)
+    wp = plan.pack(tcbf.WEIGHTS, w)
+    if prec == "f16":
+        assert "tmem" in plan.raw_variant
+        run = lambda: plan.beamform_raw(wp, x)                                   # noqa: E731
+    else:
+        assert "tmem" in plan.variant
+        xp = plan.pack(tcbf.DATA, x)
+        run = lambda: plan.beamform(wp, xp)                                      # noqa: E731
+    ref = run()
+    for _ in range(6):
+        y = run()
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref)
