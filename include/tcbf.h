@@ -117,8 +117,8 @@ tcbf_status tcbf_pack(const tcbf_plan* plan, tcbf_operand operand, const float* 
  * out: tcbf_output_bytes() bytes, 16-byte aligned, must not overlap the inputs.
  * F16: fp32 result of fp16 inputs with fp32 accumulation (tcgen05 tensor cores).
  * B1:  exact int32 result (the packed bits are expanded to +-1 and multiplied on the fp4 tensor
- *      cores, exact for K <= 2^23, int8 tensor cores beyond; for K <= 768 and
- *      M > 64 each 128-sample unit's expanded data stays in tensor memory for all beam tiles).
+ *      cores, exact for K <= 2^23, int8 tensor cores beyond; for 256 < K <= 768
+ *      and M > 64 each 128-sample unit's expanded data stays in tensor memory for all beam tiles).
  * One launch, or two (memset + kernel) when a split-K variant is forced.  One call may be in
  * flight per (plan, out) pair; the plan itself is stateless and may be used from several streams. */
 tcbf_status tcbf_beamform(const tcbf_plan* plan, const void* w_packed, const void* x_packed,

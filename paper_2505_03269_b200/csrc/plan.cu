@@ -173,10 +173,11 @@ void choose_kernels(tcbf_plan* p) {
   if (v >= 0 && v < tcbf::F16_V_COUNT) p->f16_variant = v;
 
   // 1-bit: +-1 fp4 (kind::mxf4) tensor cores, exact while 32 Kw <= 2^23; int8 AND form beyond;
-  // short K (Kw <= 24) with more than 64 beams: the sample-major kernel with the unit's data
-  // resident in TMEM and line-store epilogue (radio 1-bit GEMM 1.73-1.91 -> 1.51-1.54 ms)
+  // 2-3 K blocks (256 < K <= 768) with more than 64 beams: the sample-major kernel with the unit's
+  // data resident in TMEM and line-store epilogue (radio 1-bit GEMM 1.73-1.91 -> 1.51-1.54 ms; at
+  // one K block the beam-major kernel is faster: 372-385 vs 425-440 us for 2.15 GB of output)
   p->b1_kernel = tcbf::gemm_b1_f4_supported(p->kp) ? TCBF_B1K_F4 : TCBF_B1K_I8;
-  if (tcbf::gemm_b1_tmem_supported(p->kp) && p->M > 64) p->b1_kernel = TCBF_B1K_TMEM;
+  if (tcbf::gemm_b1_tmem_supported(p->kp) && p->kp > 8 && p->M > 64) p->b1_kernel = TCBF_B1K_TMEM;
   if (const char* e = getenv("TCBF_B1_KERNEL")) {
     if (strcmp(e, "popc") == 0) p->b1_kernel = TCBF_B1K_POPC;
     else if (strcmp(e, "i8") == 0) p->b1_kernel = TCBF_B1K_I8;

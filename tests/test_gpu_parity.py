@@ -532,7 +532,7 @@ def test_abi_errors_on_device(tcbf):
 @pytest.fixture(params=["f4", "tmem", "i8", "popc", "bmma"])
 def b1_kernel(request, monkeypatch):
     """All 1-bit kernels: tcgen05 kind::mxf4 on +-1 (beam-major, and the sample-major kernel with
-    the unit's data resident in TMEM -- the default for Kw <= 24 and M > 64; other shapes fall back
+    the unit's data resident in TMEM -- the default for 8 < Kw <= 24 and M > 64; other shapes fall back
     to the beam-major one), tcgen05 kind::i8 AND form (beyond
     the fp32-exact K range, and split-K), the CUDA-core XOR/popc kernel and the legacy b1 mma.sync
     single-AND kernel."""
