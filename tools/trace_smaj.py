@@ -16,7 +16,7 @@ from paper_2505_03269_b200 import build as _b  # noqa: E402
 import synth  # noqa: E402
 
 tcbf.library_path = os.environ.get("TRACE_LIB") or _b.build_tcbf(dev=True)  # TRACE_LIB: a variant build
-M, N, K, B = 1024, 1024, 256, 256
+M, N, K, B = 1024, 1024, int(os.environ.get("TRACE_K", "256")), 256
 plan = tcbf.Plan(M, N, K, B, "f16")
 wp = plan.pack(tcbf.WEIGHTS, synth.generate_device("phase", 1, 0, B, M, K))
 x = synth.generate_device("adc", 1, 1, B, K, N)
