@@ -149,11 +149,12 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
  *   x_f16     device, caller-owned, read-only: [B][K][N] complex as interleaved IEEE binary16
  *             pairs (re, im) -- 4 bytes per sample, N contiguous, 16-byte aligned.
  *   out       device [B][2][M][N] fp32 (plane 0 = Re, 1 = Im), 16-byte aligned.
- * The data is read as a real K x 2N matrix: two real GEMMs per K step (A_r X, A_i X) and the
- * epilogue recombines Re = (A_r X)[2n] - (A_i X)[2n+1], Im = (A_r X)[2n+1] + (A_i X)[2n].  Same
- * exact fp16 products and fp32 accumulation as tcbf_beamform; the final combination of the two
- * accumulators is one more fp32 rounding (within the 16-bit tolerance, not bit-identical).
- * Asynchronous on `stream`; one kernel launch. */
+ * For round_up(K, 64) <= 256 the (re, im) pairs are taken by TMA and split into the re / im
+ * planes on chip (byte permutes, no rounding) into the data-in-TMEM kernel: the same products and
+ * K order as tcbf_beamform_raw.  For longer K (or TCBF_F16I=res) the data is read as a real
+ * K x 2N matrix: two real GEMMs per K step (A_r X, A_i X), and the epilogue recombines
+ * Re = (A_r X)[2n] - (A_i X)[2n+1], Im = (A_r X)[2n+1] + (A_i X)[2n], one more fp32 rounding
+ * (within the 16-bit tolerance, not bit-identical).  Asynchronous on `stream`; one kernel launch. */
 tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, const void* x_f16, void* out,
                                void* stream);
 
