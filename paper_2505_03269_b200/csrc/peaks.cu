@@ -17,6 +17,8 @@
 //  10  tcgen05.mma kind::mxf4  M=128 N=128 K=64, A from TMEM (swapped kernel, TM=64)
 //  11  tcgen05.mma kind::f16   M=128 N=128 K=16, A from TMEM
 //  12  the data-in-TMEM radio kernel's K step: N=128 + N=64 (negate B) + N=64, A from TMEM
+//  13  tcgen05.mma kind::f16   M=128 N=32 K=16, A from TMEM
+//  14  the same K step for 32-beam tiles: N=64 + 2 x N=32, A from TMEM
 // (every tensor kind issued from a converged warp through elect.sync since round 2)
 // Ops are counted as 2 per multiply-accumulate (binary MACs for kinds 0-2).  Host entry point:
 // tcbf_peak_run (extern "C"), timed with CUDA events around one launch after a warm-up launch.
@@ -170,6 +172,8 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
     if (KIND == 3) idesc = idesc_f16(128, 256, false);
     else if (KIND == 6) idesc = idesc_f16(128, 64, false);
     else if (KIND == 11 || KIND == 12) idesc = idesc_f16(128, 128, false);
+    else if (KIND == 13) idesc = idesc_f16(128, 32, false);
+    else if (KIND == 14) idesc = idesc_f16(128, 64, false);
     else if (KIND == 7) idesc = idesc_f16(128, 128, false);
     else if (KIND == 4) idesc = idesc_s8(128, 256);
     else idesc = (1u << 7) | (1u << 10) | (((KIND == 8 || KIND == 9 ? 64u : KIND == 10 ? 128u : 256u) >> 3) << 17) |
@@ -179,6 +183,15 @@ __global__ void __launch_bounds__(128, 1) peak_tc_kernel(int iters, int32_t* sin
       for (int kk = 0; kk < 4; ++kk) {  // 4 x 32 bytes of K per 128-byte row
         const uint64_t ad = smem_desc_k128(sA, kk * 32), bd = smem_desc_k128(sB, kk * 32);
         if (!elect_one()) continue;
+        if (KIND == 14) {  // the same K step for 32-beam tiles: N=64 + 2 x N=32
+          constexpr uint32_t I32 = idesc_f16(128, 32, false), I32N = idesc_f16(128, 32, false) | (1u << 14);
+          const uint64_t bw = smem_desc_k128(sB, kk * 32), bwi = bw + (uint64_t)((32 * 128) >> 4);
+          mma_f16_ts_peak(tmem + 256, tmem + kk * 8, bw, idesc);
+          mma_f16_ts_peak(tmem + 256, tmem + 128 + kk * 8, bwi, I32N);
+          mma_f16_ts_peak(tmem + 256 + 32, tmem + 128 + kk * 8, bw, I32);
+          continue;
+        }
+        if (KIND == 13) { mma_f16_ts_peak(tmem + 256, tmem + kk * 8, bd, idesc); continue; }
         if (KIND == 12) {  // the data-in-TMEM radio kernel's K step: [Re|Im] += X_r [W_r;W_i], Re -= X_i W_i, Im += X_i W_r
           constexpr uint32_t I64 = idesc_f16(128, 64, false), I64N = idesc_f16(128, 64, false) | (1u << 14);
           const uint64_t bw = smem_desc_k128(sB, kk * 32), bwi = bw + (uint64_t)((64 * 128) >> 4);
@@ -225,7 +238,7 @@ extern "C" {
 // -1 for an unknown kind or iters <= 0, else the cudaError_t value.
 __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, double* seconds, double* ops) {
   using namespace tcbf;
-  if (kind < 0 || kind > 12 || iters <= 0 || !seconds || !ops) return -1;
+  if (kind < 0 || kind > 14 || iters <= 0 || !seconds || !ops) return -1;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -253,12 +266,14 @@ __attribute__((visibility("default"))) int tcbf_peak_run(int kind, int iters, do
     } else {
       auto k = kind == 3 ? peak_tc_kernel<3> : kind == 4 ? peak_tc_kernel<4> : kind == 5 ? peak_tc_kernel<5>
              : kind == 6 ? peak_tc_kernel<6> : kind == 7 ? peak_tc_kernel<7> : kind == 8 ? peak_tc_kernel<8>
-             : kind == 9 ? peak_tc_kernel<9> : kind == 10 ? peak_tc_kernel<10> : kind == 11 ? peak_tc_kernel<11> : peak_tc_kernel<12>;
+             : kind == 9 ? peak_tc_kernel<9> : kind == 10 ? peak_tc_kernel<10> : kind == 11 ? peak_tc_kernel<11> : kind == 12 ? peak_tc_kernel<12>
+             : kind == 13 ? peak_tc_kernel<13> : peak_tc_kernel<14>;
       cudaError_t a = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
       if (a != cudaSuccess) return a;
       k<<<sms, 128, TC_SMEM>>>(iters, sink);
       const double kdim = (kind == 3 || kind == 6 || kind == 7 || kind >= 11) ? 16 : kind == 4 ? 32 : 64;
-      const double ndim = (kind == 6 || kind == 8 || kind == 9) ? 64 : (kind == 7 || kind == 10 || kind == 11) ? 128 : 256;
+      const double ndim = (kind == 6 || kind == 8 || kind == 9) ? 64 : (kind == 7 || kind == 10 || kind == 11 || kind == 14) ? 128
+                         : kind == 13 ? 32 : 256;
       work = 2.0 * 128 * ndim * kdim * 4 * (double)iters * sms;
     }
     return cudaGetLastError();

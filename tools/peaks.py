@@ -35,10 +35,12 @@ KINDS = {
     10: ("tcgen05_mxf4_ts_n128", "tcgen05.mma kind::mxf4 block32 128x128x64, A from TMEM", 1.0),
     11: ("tcgen05_f16_ts_n128", "tcgen05.mma kind::f16 128x128x16, A from TMEM", 1.0),
     12: ("tcgen05_f16_ts_radio_step", "kind::f16 N=128 + N=64 (negate B) + N=64, A from TMEM (radio K step)", 1.0),
+    13: ("tcgen05_f16_ts_n32", "tcgen05.mma kind::f16 128x32x16, A from TMEM", 1.0),
+    14: ("tcgen05_f16_ts_radio_step_32beams", "kind::f16 N=64 + 2 x N=32, A from TMEM (32-beam K step)", 1.0),
 }
 # iterations per warp / issuing thread: each launch runs ~5-50 ms
 ITERS = {0: 4000, 1: 4000, 2: 20000, 3: 40000, 4: 40000, 5: 40000, 6: 80000, 7: 80000, 8: 80000, 9: 80000,
-         10: 80000, 11: 80000, 12: 40000}
+         10: 80000, 11: 80000, 12: 40000, 13: 160000, 14: 80000}
 
 
 def clocks():
