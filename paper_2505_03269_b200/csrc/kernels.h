@@ -70,6 +70,11 @@ int gemm_f16_tmem_beams();
 int gemm_f16_tmem_raw_rows();
 cudaError_t launch_gemm_f16_tmem(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
                                  int layout, int wkb, int cluster, int num_sms, cudaStream_t stream);
+// the same with 32-beam tiles and half of the next unit staged in TMEM (gemm_f16_tmem2.cu): K16 == 256
+bool gemm_f16_tmem2_supported(int64_t K16);
+int gemm_f16_tmem2_beams();
+cudaError_t launch_gemm_f16_tmem2(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmF16Args& args,
+                                  int layout, int wkb, int cluster, int num_sms, cudaStream_t stream);
 struct GemmB1Args;
 // 1-bit sample-major kernel with the unit's expanded data resident in TMEM (gemm_b1_tmem.cu):
 // Kw <= 24 words; 64-beam tiles, 128-sample units, line-store epilogue (any N)

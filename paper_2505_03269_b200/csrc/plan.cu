@@ -219,9 +219,17 @@ void choose_kernels(tcbf_plan* p) {
   // (the TMEM kernel takes the raw data by TMA: 16-byte rows need N % 4 == 0 in either layout;
   // other N take the smem sample-major kernel, chosen here so the plan's kernel name holds)
   p->f16_fused_kind = p->N % 4 == 0 ? TCBF_FUSED_TMEM : TCBF_FUSED_SMAJ;
+  // K16 = 256 (the radio shape class): 32-beam tiles, half of the next unit written straight into
+  // TMEM, the freed staging spent on a deeper weight ring (gemm_f16_tmem2.cu; TCBF_F16_FUSED=tmem
+  // keeps the 64-beam kernel); WKB 4 (one 32 KB stage per tile) measured fastest
+  const int tmem32_wkb = env_int("TCBF_TMEM2_WKB", 4) == 2 ? 2 : 4;
+  p->tmem32 = tcbf::gemm_f16_tmem2_supported(p->kp) ? tmem32_wkb : 0;
   if (const char* e = getenv("TCBF_F16_FUSED")) {
     if (strcmp(e, "smaj") == 0) p->f16_fused_kind = TCBF_FUSED_SMAJ;
-    else if (strcmp(e, "tmem") == 0 && p->N % 4 == 0) p->f16_fused_kind = TCBF_FUSED_TMEM;
+    else if (strcmp(e, "tmem") == 0 && p->N % 4 == 0) {
+      p->f16_fused_kind = TCBF_FUSED_TMEM;
+      p->tmem32 = 0;
+    }
   }
   p->tmem_wkb = env_int("TCBF_TMEM_WKB", 1) == 2 ? 2 : 1;  // K blocks per weight stage
   // weight multicast cluster of the sample-major kernel (TCBF_F16_MC=0 turns multicast off)
@@ -516,13 +524,15 @@ const char* tcbf_plan_kernel(const tcbf_plan* plan, tcbf_entry entry) {
     case TCBF_ENTRY_BEAMFORM: return gemm_kernel_name(plan);
     case TCBF_ENTRY_BEAMFORM_RAW:
       if (plan->raw_mode == TCBF_RAW_FUSED)
-        return plan->f16_fused_kind == TCBF_FUSED_TMEM ? "f16_tcgen05_fused_tmem_128x64"
+        return plan->f16_fused_kind == TCBF_FUSED_TMEM ? (plan->tmem32 ? "f16_tcgen05_fused_tmem_128x32"
+                                                                        : "f16_tcgen05_fused_tmem_128x64")
                                                        : "f16_tcgen05_fused_smaj_128x128";
       if (plan->raw_mode == TCBF_RAW_STREAM) return "f16_tcgen05_stream_conv_128x128";
       return gemm_kernel_name(plan);  // preceded by the pack kernel
     case TCBF_ENTRY_BEAMFORM_F16I:
       return plan->prec != TCBF_PREC_F16 ? "none"
-             : plan->f16i_tmem     ? "f16_tcgen05_interleaved_tmem_128x64"
+             : plan->f16i_tmem     ? (plan->tmem32 ? "f16_tcgen05_interleaved_tmem_128x32"
+                                                   : "f16_tcgen05_interleaved_tmem_128x64")
              : plan->f16i_resident ? "f16_tcgen05_interleaved_resident_128x64" : "f16_tcgen05_interleaved_smaj_64x128";
   }
   return "none";
@@ -586,8 +596,9 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
   if (plan->raw_mode == TCBF_RAW_FUSED && plan->f16_fused_kind == TCBF_FUSED_TMEM && tmem_tma_ok) {
     // weights: the stacked K-major B operand, boxes {64 K, 64 beams} of a plane, 128-byte swizzle
     CUtensorMap tw, tx;
-    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 64,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    const int bn = plan->tmem32 ? tcbf::gemm_f16_tmem2_beams() : tcbf::gemm_f16_tmem_beams();
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64,
+                  (uint32_t)bn, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
     const uint32_t rr = (uint32_t)tcbf::gemm_f16_tmem_raw_rows();
     if (layout == TCBF_SRC_INTERLEAVED)
@@ -599,9 +610,8 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
     if (s != TCBF_OK) return s;
     tcbf::GemmF16Args a;
     memset(&a, 0, sizeof(a));
-    const int bn = tcbf::gemm_f16_tmem_beams();
     a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
-    a.tiles_m = (int)((plan->M + bn - 1) / bn);  // 64-beam tiles
+    a.tiles_m = (int)((plan->M + bn - 1) / bn);  // 64- (32-) beam tiles
     a.tiles_n = (int)((plan->N + 127) / 128);    // 128-sample units per batch entry
     a.num_kb = (int)(plan->kp / 64);
     const int64_t nu = (int64_t)a.tiles_n * plan->B;
@@ -616,7 +626,10 @@ tcbf_status tcbf_beamform_raw(const tcbf_plan* plan, const void* w_packed, const
       cudaMemsetAsync(a.trace, 0, (size_t)plan->num_sms * 1024 * 8, st);
     }
 #endif
-    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, (int)layout, plan->tmem_wkb, plan->smaj_cluster, plan->num_sms, st);
+    cudaError_t e = plan->tmem32 ? tcbf::launch_gemm_f16_tmem2(tw, tx, a, (int)layout, plan->tmem32, plan->smaj_cluster,
+                                                            plan->num_sms, st)
+                                 : tcbf::launch_gemm_f16_tmem(tw, tx, a, (int)layout, plan->tmem_wkb, plan->smaj_cluster,
+                                                           plan->num_sms, st);
 #ifdef TCBF_DEV
     if (trace_file) {
       std::vector<unsigned long long> h((size_t)plan->num_sms * 1024);
@@ -754,8 +767,9 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
     // data-in-TMEM kernel with the fp16 pairs by TMA ({N, K, B} 32-bit elements, 16-row boxes),
     // de-interleaved into the staged next unit (DESIGN.md §4 NEXT-1)
     CUtensorMap tw, tx;
-    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64, 64,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+    const int bn = plan->tmem32 ? tcbf::gemm_f16_tmem2_beams() : tcbf::gemm_f16_tmem_beams();
+    s = encode_3d(&tw, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, w_packed, plan->kp, plan->M, 2 * plan->B, 64,
+                  (uint32_t)bn, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     if (s != TCBF_OK) return s;
     s = encode_3d(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, x_f16, plan->N, plan->K, plan->B, 128,
                   (uint32_t)tcbf::gemm_f16_tmem_raw_rows(), CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -763,7 +777,6 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
     if (s != TCBF_OK) return s;
     tcbf::GemmF16Args a;
     memset(&a, 0, sizeof(a));
-    const int bn = tcbf::gemm_f16_tmem_beams();
     a.M = (int)plan->M; a.N = (int)plan->N; a.B = (int)plan->B; a.K16 = (int)plan->kp;
     a.tiles_m = (int)((plan->M + bn - 1) / bn);
     a.tiles_n = (int)((plan->N + 127) / 128);
@@ -773,7 +786,10 @@ tcbf_status tcbf_beamform_f16i(const tcbf_plan* plan, const void* w_packed, cons
     a.num_tiles = (int)(nu * a.tiles_m);
     a.out = static_cast<float*>(out);
     a.debug = plan->debug;
-    cudaError_t e = tcbf::launch_gemm_f16_tmem(tw, tx, a, 2, plan->tmem_wkb, plan->smaj_cluster, plan->num_sms, st);
+    cudaError_t e = plan->tmem32 ? tcbf::launch_gemm_f16_tmem2(tw, tx, a, 2, plan->tmem32, plan->smaj_cluster,
+                                                            plan->num_sms, st)
+                                 : tcbf::launch_gemm_f16_tmem(tw, tx, a, 2, plan->tmem_wkb, plan->smaj_cluster,
+                                                           plan->num_sms, st);
     if (e != cudaSuccess) return cuda_fail(e, "interleaved-fp16 (data in TMEM) beamform kernel launch");
     g_launches = 1;
     return TCBF_OK;

@@ -29,6 +29,7 @@ struct tcbf_plan_s {
   int f16i_tmem;      // tcbf_beamform_f16i: the data-in-TMEM kernel (K16 <= 256), preferred over both
   int smaj_cluster;   // sample-major fused kernel: weight-multicast cluster size (1 or 2)
   int tmem_wkb;       // data-in-TMEM fused kernel: K blocks per weight stage (1 or 2)
+  int tmem32;         // data-in-TMEM fused kernel with 32-beam tiles (gemm_f16_tmem2.cu): 0, or its WKB (2/4)
   int raw_mode;       // TCBF_RAW_*: what tcbf_beamform_raw runs
   int conv_splits_override;  // streaming-conversion K split (0 = by shape)
   int b1_kernel;      // TCBF_B1K_*: fp4 +-1 tensor cores (default), int8 AND form, legacy b1 mma.sync, popc

@@ -300,7 +300,8 @@ def test_f16_beamform_raw_split_k(tcbf, shape, splits, monkeypatch):
 
 # ------------------------------------------------------------------ fp16 interleaved data, no pack (NEXT-1)
 @pytest.mark.parametrize("shape", [(8, 64, 32, 2), (200, 300, 100, 3), (130, 136, 64, 3), (300, 1000, 480, 2),
-                                   (1024, 1024, 256, 2), (1000, 260, 333, 1), (64, 4, 16, 1), (96, 520, 200, 90)])
+                                   (1024, 1024, 256, 2), (1000, 260, 333, 1), (64, 4, 16, 1), (96, 520, 200, 90),
+                                   (40, 512, 256, 160)])
 @pytest.mark.parametrize("kernel", ["default", "res", "stream"])
 def test_f16i_interleaved_fp16_beamform(tcbf, shape, kernel, monkeypatch):
     """tcbf_beamform_f16i on fp16 interleaved data: the default data-in-TMEM kernel (pairs
@@ -357,7 +358,7 @@ def test_f16i_resident_equals_streaming(tcbf, shape, monkeypatch):
     y_res = plan.beamform_f16i(wp, xd)
     monkeypatch.delenv("TCBF_F16I")
     pt = tcbf.Plan(M, N, K, B, "f16")
-    assert pt.kernel("f16i") == "f16_tcgen05_interleaved_tmem_128x64", pt.kernel("f16i")
+    assert pt.kernel("f16i").startswith("f16_tcgen05_interleaved_tmem_128x"), pt.kernel("f16i")
     y_tmem = pt.beamform_f16i(wp, xd)
     monkeypatch.setenv("TCBF_F16I_STREAM", "1")
     ps = tcbf.Plan(M, N, K, B, "f16")
@@ -775,9 +776,10 @@ def test_full_size_radio_b1_sampled(tcbf, b1_kernel):
 
 def test_full_size_radio_f16_raw_sampled(tcbf):
     """BASELINE configs[1] through tcbf_beamform_raw, the launch bench.py times (data-in-TMEM fused
-    kernel: 2048 units on 148 CTAs, the data of each next unit staged in smem, raw data by TMA)."""
+    kernel with 32-beam tiles: 2048 units on 148 CTAs, half of each next unit written straight
+    into TMEM, raw data by TMA)."""
     plan = tcbf.Plan(1024, 1024, 256, 256, "f16")
-    assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x64", plan.raw_variant
+    assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x32", plan.raw_variant
     _full_size(tcbf, "f16", 1024, 1024, 256, 256, "phase", "adc", synth.SEED_BASE + 1,
                batches=[0, 77, 255], rows=[0, 63, 64, 127, 128, 700, 1023], path="raw")
 
@@ -801,15 +803,50 @@ def test_f16_tmem_fused_kernel_odd_n_plan(tcbf):
 
 
 @pytest.mark.parametrize("shape", TMEM_SHAPES)
-def test_f16_tmem_fused_kernel(tcbf, shape):
-    """The data-in-TMEM fused kernel equals pack + beamform up to fp32 summation order inside the
-    MMA and meets the oracle on sampled batch entries."""
+def test_f16_tmem_fused_kernel(tcbf, shape, monkeypatch):
+    """The data-in-TMEM fused kernel (64-beam tiles, forced for K16 = 256 too) equals pack +
+    beamform up to fp32 summation order inside the MMA and meets the oracle on sampled batch
+    entries."""
     M, N, K, B, layout = shape
+    monkeypatch.setenv("TCBF_F16_FUSED", "tmem")
     w = synth.generate("phase", 37, 0, B, M, K)
     x = synth.generate("adc", 37, 1, B, K, N)
     conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
     plan = tcbf.Plan(M, N, K, B, "f16")
     assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x64", plan.raw_variant
+    wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
+    xd = _dev(conv(x))
+    y_raw = plan.beamform_raw(wp, xd, layout)
+    y_ref = plan.beamform(wp, plan.pack(tcbf.DATA, xd, layout))
+    torch.cuda.synchronize()
+    assert (y_raw - y_ref).abs().max().item() <= 1e-6 * y_ref.abs().max().item()
+    sel = sorted({0, B // 2, B - 1})
+    ref = oracle.cgemm_f16(conv(w[sel]), conv(x[sel]), 0 if layout == "interleaved" else 1, M, N, K, len(sel))
+    _check_f16(y_raw[sel].cpu().numpy(), ref, w[sel], x[sel])
+
+
+# the 32-beam-tile variant (K16 = 256; half of the next unit written straight into TMEM, three
+# rotating data regions): >= 4 units per CTA so every region is reused, ragged M and N, both
+# layouts, with and without the CTA-pair weight multicast (tiles_n odd -> no pairs), WKB 2 and 4
+TMEM32_SHAPES = [
+    (130, 520, 200, 160, "interleaved", "2"),
+    (96, 512, 256, 160, "planar", "2"),
+    (33, 256, 193, 300, "interleaved", "4"),
+    (1024, 1024, 256, 12, "planar", "4"),
+]
+
+
+@pytest.mark.parametrize("shape", TMEM32_SHAPES)
+def test_f16_tmem32_fused_kernel(tcbf, shape, monkeypatch):
+    """The 32-beam data-in-TMEM kernel (the K16 = 256 default) equals pack + beamform up to fp32
+    summation order and meets the oracle on sampled batch entries."""
+    M, N, K, B, layout, wkb = shape
+    monkeypatch.setenv("TCBF_TMEM2_WKB", wkb)
+    w = synth.generate("phase", 41, 0, B, M, K)
+    x = synth.generate("adc", 41, 1, B, K, N)
+    conv = synth.to_interleaved if layout == "interleaved" else synth.to_planar
+    plan = tcbf.Plan(M, N, K, B, "f16")
+    assert plan.raw_variant == "f16_tcgen05_fused_tmem_128x32", plan.raw_variant
     wp = plan.pack(tcbf.WEIGHTS, _dev(conv(w)), layout)
     xd = _dev(conv(x))
     y_raw = plan.beamform_raw(wp, xd, layout)
