@@ -23,7 +23,8 @@ elif os.environ.get("AB_DEV_LIB"):   # ablation studies: the TCBF_DEV build (TCB
     from paper_2505_03269_b200 import build as _b
     tcbf.library_path = _b.build_tcbf(dev=True)
 
-VARIANTS = [("tmem", {}), ("tmem_nomc", {"TCBF_F16_MC": "0"}), ("smaj", {"TCBF_F16_FUSED": "smaj"})]
+VARIANTS = [("tmem", {}), ("tmem64", {"TCBF_F16_FUSED": "tmem"}), ("tmem_nomc", {"TCBF_F16_MC": "0"}),
+            ("smaj", {"TCBF_F16_FUSED": "smaj"})]   # tmem = the plan default (32-beam tiles at K16 = 256)
 if os.environ.get("AB_VARIANTS"):   # e.g. "smaj8:,nostore:TCBF_DEBUG=1,nomma:TCBF_DEBUG=2"
     VARIANTS = []
     for item in os.environ["AB_VARIANTS"].split(","):
